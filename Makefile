@@ -1,0 +1,54 @@
+# Top-level build: the product library (sm_100a CUDA + C-ABI + C++ drop-in)
+# and the test-only oracle.  `python -c "import __graft_entry__ as g; g.build()"`
+# runs this.  cudart is linked statically and the driver API is resolved at
+# run time, so libtw.so loads on GPU-less hosts.
+
+NVCC ?= nvcc
+CXX ?= g++
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := -std=c++17 -O3 -lineinfo $(ARCH) -Xcompiler -fPIC -Xcompiler -fvisibility=hidden \
+           -Iinclude -Ipaper_2505_11329_b200/csrc -Xptxas -warn-spills
+PKG := paper_2505_11329_b200
+LIBDIR := $(PKG)/lib
+OBJDIR := build/obj
+
+KSRC := $(PKG)/csrc/kernels/tw_launch.cu
+HSRC := $(PKG)/csrc/host/tw_capi.cu
+KHDR := $(wildcard $(PKG)/csrc/kernels/*.cuh) $(PKG)/csrc/kernels/tw_launch.h
+HHDR := $(PKG)/csrc/host/tw_internal.h include/tw/tw.h
+SHIM_SRC := $(wildcard $(PKG)/csrc/host/weavesim_*.cpp)
+SHIM_HDR := $(wildcard include/weavesim/*.hpp)
+
+.PHONY: all lib shim oracle ref clean
+
+all: lib shim oracle
+
+lib: $(LIBDIR)/libtw.so
+
+$(OBJDIR)/tw_launch.o: $(KSRC) $(KHDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(OBJDIR)/tw_capi.o: $(HSRC) $(HHDR) $(KHDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIBDIR)/libtw.so: $(OBJDIR)/tw_launch.o $(OBJDIR)/tw_capi.o
+	@mkdir -p $(LIBDIR)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -Xlinker --exclude-libs,ALL
+
+# The drop-in C++ API (namespace weavesim) over the C-ABI.
+shim: $(LIBDIR)/libweavesim_b200.so
+
+$(LIBDIR)/libweavesim_b200.so: $(SHIM_SRC) $(SHIM_HDR) $(LIBDIR)/libtw.so
+	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -o $@ $(SHIM_SRC) -L$(LIBDIR) -ltw -Wl,-rpath,'$$ORIGIN' -pthread
+
+oracle:
+	$(MAKE) -C oracle oracle
+
+ref:
+	$(MAKE) -C oracle ref
+
+clean:
+	rm -rf build $(LIBDIR)
+	$(MAKE) -C oracle clean

@@ -1,0 +1,151 @@
+/*
+ * tw.h -- C-ABI of the B200-native TokenWeave hot path (libtw.so).
+ *
+ * Plain pointers and sizes only; no torch or C++ types cross this boundary.
+ * Device pointers are CUDA device addresses on the rank's device; `stream`
+ * arguments are cudaStream_t passed as void* (NULL = legacy default stream).
+ *
+ * Every entry point below replaces a reference interface (paths relative to
+ * /root/reference); the drop-in C++ API (include/weavesim/*.hpp) is layered
+ * on top of these calls and keeps the reference signatures and exceptions.
+ *
+ * Threading: a communicator is not safe for concurrent mutation (the
+ * reference's RankGroup contract); callers serialise calls on a
+ * given tw_comm_t.  tw_last_error() is thread-local.
+ */
+#ifndef TW_TW_H
+#define TW_TW_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TW_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define TW_API __attribute__((visibility("default")))
+#else
+#define TW_API
+#endif
+
+/* Status codes.  The first four map 1:1 onto the reference exception
+ * taxonomy (proj/include/weavesim/errors.hpp:8-23). */
+typedef enum tw_status {
+  TW_OK = 0,
+  TW_ERR_DIMENSION = 1,   /* weavesim::DimensionError  errors.hpp:8   */
+  TW_ERR_NUMERIC = 2,     /* weavesim::NumericError    errors.hpp:12  */
+  TW_ERR_CONFIG = 3,      /* weavesim::ConfigError     errors.hpp:16  */
+  TW_ERR_CONTRACT = 4,    /* weavesim::ContractError   errors.hpp:21  */
+  TW_ERR_CUDA = 5,        /* CUDA runtime/driver failure              */
+  TW_ERR_TIMEOUT = 6,     /* cross-rank barrier did not complete      */
+  TW_ERR_UNSUPPORTED = 7  /* e.g. NVLS requested on a non-NVSwitch box */
+} tw_status;
+
+/* Activation storage type.  Weights are always fp32 (NormParams::weight is
+ * std::vector<float>, proj/include/weavesim/numerics.hpp:27-30). */
+typedef enum tw_dtype { TW_BF16 = 0, TW_F32 = 1 } tw_dtype;
+
+/* Transport of the fused collective.
+ *  NVLS : NVSwitch multicast object (cuMulticastCreate/BindMem); reduce-
+ *         scatter with multimem.ld_reduce, all-gather with multimem.st.
+ *  PEER : unicast loads/stores on every rank's mapped buffer (NVLink P2P
+ *         between GPUs, or plain HBM when several simulated ranks share one
+ *         device -- the reference's in-process RankGroup, collectives.hpp:34).
+ *  AUTO : NVLS when every rank is on a distinct multicast-capable device,
+ *         PEER otherwise. */
+typedef enum tw_transport { TW_TRANSPORT_AUTO = 0, TW_TRANSPORT_NVLS = 1, TW_TRANSPORT_PEER = 2 } tw_transport;
+
+/* Symmetric buffers owned by a communicator (one per rank, same size). */
+typedef enum tw_buffer {
+  TW_BUF_INPUT = 0,    /* [T,H] partial sums the producer GEMM writes (RankGroup::inputs)      */
+  TW_BUF_OUTPUT = 1,   /* [T,H] replicated normed output (fused_allreduce_rmsnorm's return)    */
+  TW_BUF_RESIDUAL = 2  /* [T,H] replicated updated residual (TW_GATHER_RESIDUAL only)           */
+} tw_buffer;
+
+/* Flags for the fused op. */
+#define TW_GATHER_RESIDUAL 0x1u /* G=2: all-gather r' as well as the output  */
+#define TW_CHECK_FINITE 0x2u    /* device-side NaN/Inf scan -> TW_ERR_NUMERIC */
+
+typedef struct tw_comm* tw_comm_t;
+
+/* Library identification. */
+TW_API int tw_abi_version(void);
+TW_API const char* tw_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+TW_API const char* tw_last_error(void);
+/* Number of CUDA devices visible (0 on a host without a GPU; never fails). */
+TW_API int tw_device_count(void);
+
+/* --- TP = 1: fused residual-add + RMSNorm (kernel K2) -----------------------
+ * Replaces weavesim::rmsnorm_residual (proj/include/weavesim/numerics.hpp:42-43,
+ * proj/src/numerics.cpp:30-64):
+ *   residual_out = input + residual;  output = residual_out * rsqrt(mean(residual_out^2)+eps) * weight
+ * input/residual/residual_out/output are [T,H] row-major of `dtype`; weight is
+ * fp32[H].  residual_out may alias residual (in-place update); no other
+ * aliasing.  sm_budget <= 0 means "whole GPU".  Shape errors -> DIMENSION,
+ * eps < 0 or NaN -> NUMERIC (numerics.cpp:43-45). */
+TW_API tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* residual_out, void* output,
+                              const float* weight, int64_t T, int64_t H, float eps, tw_dtype dtype,
+                              int sm_budget, void* stream);
+
+/* Device-side finite scan: *nonfinite_count (device int32) += #NaN/Inf in x.
+ * Replaces TokenMatrix::validate's isfinite loop (numerics.cpp:25-27). */
+TW_API tw_status tw_count_nonfinite(const void* x, int64_t n, tw_dtype dtype, int* nonfinite_count_dev, void* stream);
+
+/* --- Token shard map (host, integer) -----------------------------------------
+ * Replaces weavesim::token_shard_map (proj/src/collectives.cpp:26-39) and
+ * ShardMap::validate (:14-24).  ranges: 2*world int64 {begin,end}. */
+TW_API tw_status tw_token_shard_map(int64_t num_tokens, int world, int64_t* ranges);
+TW_API tw_status tw_shard_map_validate(const int64_t* ranges, int world, int64_t total_tokens);
+
+/* --- Communicator --------------------------------------------------------------
+ * One communicator = `world` ranks with symmetric INPUT/OUTPUT/RESIDUAL buffers
+ * of `buffer_bytes` each plus signal pads, set up once (multicast objects
+ * bound and mapped, peer pointers resolved).  devices[r] is the CUDA device of
+ * rank r; devices may repeat (simulated ranks sharing a GPU, PEER transport).
+ * Replaces the in-process RankGroup (proj/include/weavesim/collectives.hpp:36-46). */
+TW_API tw_status tw_comm_create(int world, const int* devices, size_t buffer_bytes, tw_transport transport,
+                         tw_comm_t* out);
+TW_API tw_status tw_comm_destroy(tw_comm_t comm);
+TW_API tw_status tw_comm_info(tw_comm_t comm, int* world, tw_transport* transport, size_t* buffer_bytes);
+TW_API tw_status tw_comm_buffer(tw_comm_t comm, int rank, tw_buffer which, void** device_ptr);
+/* Multicast (NVLS) address of a buffer; TW_ERR_UNSUPPORTED on PEER comms. */
+TW_API tw_status tw_comm_multicast_buffer(tw_comm_t comm, int rank, tw_buffer which, void** device_ptr);
+
+/* --- Fused AllReduce + residual-add + RMSNorm (kernel K1) ---------------------
+ * Replaces weavesim::fused_allreduce_rmsnorm (proj/include/weavesim/collectives.hpp:63-64,
+ * proj/src/collectives.cpp:157-182).  For rank r with token shard [b_r,e_r):
+ *   x      = sum over ranks of INPUT[t]          (reduce-scatter, t in shard)
+ *   r'     = x + residual_shard[t-b_r]            (residual_shard overwritten, :144)
+ *   out[t] = r' * rsqrt(mean(r'^2)+eps) * weight  -> OUTPUT[t] on every rank (all-gather)
+ *   with TW_GATHER_RESIDUAL also r' -> RESIDUAL[t] on every rank.
+ * shard_ranges: 2*world int64 (must satisfy ShardMap::validate, else CONTRACT).
+ * residual_shards[r]: device [e_r-b_r, H] of dtype on rank r's device.
+ * weights[r]: device fp32[H] on rank r's device.  streams[r]: cudaStream_t.
+ * sm_budget: CTAs per rank (1 CTA/SM), the paper's 2-16 SM knob.
+ *
+ * _group launches every rank this process owns (required when simulated ranks
+ * share a device: one launch keeps them co-resident for the in-kernel
+ * barrier).  Ranks never run partially: all must be launched. */
+TW_API tw_status tw_fused_allreduce_rmsnorm_group(tw_comm_t comm, int64_t T, int64_t H, const int64_t* shard_ranges,
+                                           void* const* residual_shards, const float* const* weights, float eps,
+                                           tw_dtype dtype, int sm_budget, unsigned flags, void* const* streams);
+
+/* --- Unfused baselines (NOT the product path) ---------------------------------
+ * all_reduce (collectives.cpp:82-88) over the communicator: OUTPUT[t] = sum_r INPUT[t]
+ * for every t (one-shot NVLS ld_reduce + multimem.st, or PEER loads). */
+TW_API tw_status tw_allreduce_group(tw_comm_t comm, int64_t T, int64_t H, tw_dtype dtype, int sm_budget,
+                             void* const* streams);
+
+/* Per-rank async error flag set by the in-kernel bounded barrier spin.
+ * Returns TW_ERR_TIMEOUT (and clears the flag) if any rank timed out. */
+TW_API tw_status tw_comm_check(tw_comm_t comm);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TW_TW_H */

@@ -1,0 +1,282 @@
+// ref_capi.cpp -- extern "C" adapter over the UNMODIFIED reference sources
+// (/root/reference/proj/src/*.cpp), compiled by oracle/Makefile into
+// oracle/_ref/libweavesim_ref.so.  TEST INFRASTRUCTURE ONLY: used by tests/
+// to pin the C restatement (tw_oracle.c) and golden fixtures, and by bench.py
+// as the reference CPU arm.  Never linked by the product.
+//
+// Exceptions from the reference API are mapped to tw.h status codes:
+// DimensionError 1, NumericError 2, ConfigError 3, ContractError 4, other 9.
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <random>
+#include <thread>
+#include <vector>
+
+#include "weavesim/collectives.hpp"
+#include "weavesim/errors.hpp"
+#include "weavesim/numerics.hpp"
+#include "weavesim/presets.hpp"
+#include "weavesim/scheduler.hpp"
+#include "weavesim/splitter.hpp"
+#include "weavesim/wavemodel.hpp"
+
+using namespace weavesim;
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const DimensionError&) {
+    return 1;
+  } catch (const NumericError&) {
+    return 2;
+  } catch (const ConfigError&) {
+    return 3;
+  } catch (const ContractError&) {
+    return 4;
+  } catch (...) {
+    return 9;
+  }
+}
+
+TokenMatrix make_matrix(const float* v, std::int64_t T, std::int64_t H) {
+  TokenMatrix m;
+  m.num_tokens = T;
+  m.hidden = H;
+  m.values.assign(v, v + T * H);
+  return m;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ref_rmsnorm_residual(const float* input, const float* residual, const float* weight,
+                         std::int64_t T, std::int64_t H, float eps, float* output,
+                         float* residual_out) {
+  return guarded([&] {
+    NormParams p;
+    p.weight.assign(weight, weight + H);
+    p.epsilon = eps;
+    NormResult r = rmsnorm_residual(make_matrix(input, T, H), make_matrix(residual, T, H), p);
+    std::memcpy(output, r.output.values.data(), sizeof(float) * T * H);
+    std::memcpy(residual_out, r.residual_out.values.data(), sizeof(float) * T * H);
+  });
+}
+
+int ref_token_shard_map(std::int64_t T, int world, std::int64_t* ranges) {
+  return guarded([&] {
+    ShardMap m = token_shard_map(T, world);
+    for (int r = 0; r < world; ++r) {
+      ranges[2 * r] = m.ranges[r].begin;
+      ranges[2 * r + 1] = m.ranges[r].end;
+    }
+  });
+}
+
+int ref_shard_map_validate(const std::int64_t* ranges, int world, std::int64_t total) {
+  return guarded([&] {
+    ShardMap m;
+    for (int r = 0; r < world; ++r) m.ranges.push_back({ranges[2 * r], ranges[2 * r + 1]});
+    m.validate(total);
+  });
+}
+
+int ref_all_reduce(int world, const float* const* inputs, std::int64_t T, std::int64_t H,
+                   float* out) {
+  return guarded([&] {
+    RankGroup g;
+    g.world_size = world;
+    for (int r = 0; r < world; ++r) g.inputs.push_back(make_matrix(inputs[r], T, H));
+    TokenMatrix s = all_reduce(g);
+    std::memcpy(out, s.values.data(), sizeof(float) * T * H);
+  });
+}
+
+// ranges == nullptr -> token_shard_map(T, world).  residual_shards[r] is
+// [T_r, H] and receives r' (the reference overwrites its shards).
+int ref_fused_allreduce_rmsnorm(int world, const float* const* inputs, float* const* residual_shards,
+                                const std::int64_t* ranges, const float* weight, std::int64_t T,
+                                std::int64_t H, float eps, int parallel, float* output) {
+  return guarded([&] {
+    RankGroup g;
+    g.world_size = world;
+    for (int r = 0; r < world; ++r) g.inputs.push_back(make_matrix(inputs[r], T, H));
+    ShardMap shards;
+    if (ranges) {
+      for (int r = 0; r < world; ++r) shards.ranges.push_back({ranges[2 * r], ranges[2 * r + 1]});
+    } else {
+      shards = token_shard_map(T, world);
+    }
+    for (int r = 0; r < world; ++r) {
+      const std::int64_t len = std::max<std::int64_t>(0, shards.ranges[r].size());
+      g.residual_shards.push_back(make_matrix(residual_shards[r], len, H));
+    }
+    NormParams p;
+    p.weight.assign(weight, weight + H);
+    p.epsilon = eps;
+    TokenMatrix out = fused_allreduce_rmsnorm(g, p, shards, parallel != 0);
+    std::memcpy(output, out.values.data(), sizeof(float) * T * H);
+    for (int r = 0; r < world; ++r) {
+      std::memcpy(residual_shards[r], g.residual_shards[r].values.data(),
+                  sizeof(float) * g.residual_shards[r].values.size());
+    }
+  });
+}
+
+// The acceptance-test draw order (proj/tests/acceptance.cpp:45-66):
+// mt19937_64(seed); N rank inputs U(-1,1); residual shards U(-1,1) in shard
+// order; weight U(0.5,1.5).  inputs: world*T*H, residual: T*H (shards
+// concatenated in token order), weight: H.
+void ref_fill_group(std::uint64_t seed, int world, std::int64_t T, std::int64_t H, float* inputs,
+                    float* residual, float* weight) {
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+  for (std::int64_t i = 0; i < static_cast<std::int64_t>(world) * T * H; ++i) inputs[i] = dist(rng);
+  for (std::int64_t i = 0; i < T * H; ++i) residual[i] = dist(rng);
+  std::uniform_real_distribution<float> wdist(0.5f, 1.5f);
+  for (std::int64_t j = 0; j < H; ++j) weight[j] = wdist(rng);
+}
+
+std::uint64_t ref_acceptance_seed(int world, std::int64_t T, std::int64_t H, int i) {
+  return (static_cast<std::uint64_t>(world) << 48) ^ (static_cast<std::uint64_t>(T) << 24) ^
+         (static_cast<std::uint64_t>(H) << 8) ^ static_cast<std::uint64_t>(i);
+}
+
+// Wave model and split planner (proj/src/wavemodel.cpp:38-49, splitter.cpp).
+std::int64_t ref_cta_count(std::int64_t tokens, int tile_tokens, int cta_columns) {
+  HardwareProfile p;
+  p.tile_tokens = tile_tokens;
+  p.cta_columns = cta_columns;
+  return cta_count(tokens, p);
+}
+
+std::int64_t ref_smart_offset_analytic(std::int64_t tokens, int num_sms, int tile_tokens,
+                                       int cta_columns) {
+  HardwareProfile p;
+  p.num_sms = num_sms;
+  p.tile_tokens = tile_tokens;
+  p.cta_columns = cta_columns;
+  return smart_offset_analytic(tokens, p);
+}
+
+// Builtin profile + model preset plan (Appendix A of SURVEY.md).
+// out4 = {prefix, suffix, offset, mode}.  Also returns the profile geometry
+// in geom3 = {num_sms, tile_tokens, cta_columns} and the policy threshold.
+int ref_make_split_plan(const char* profile, const char* model, std::int64_t T, std::int64_t* out4,
+                        std::int64_t* geom4) {
+  return guarded([&] {
+    HardwareProfile hp = builtin_profile(profile);
+    ModelPreset mp = model_preset(model);
+    SplitPlan plan = make_split_plan(T, hp, mp.policy);
+    out4[0] = plan.prefix_tokens;
+    out4[1] = plan.suffix_tokens;
+    out4[2] = plan.offset;
+    out4[3] = static_cast<std::int64_t>(plan.mode);
+    if (geom4) {
+      geom4[0] = hp.num_sms;
+      geom4[1] = hp.tile_tokens;
+      geom4[2] = hp.cta_columns;
+      geom4[3] = mp.policy.threshold_tokens;
+    }
+  });
+}
+
+// Modeled per-layer latency (seconds) of build_layer_graph + simulate for
+// one layer, no tail: the reference's "predicted" column.  mode is a
+// BaselineMode name ("multimem", "fuseonly", "tokenweave", ...).
+int ref_layer_latency(const char* profile, const char* model, std::int64_t T, const char* mode,
+                      double* seconds) {
+  return guarded([&] {
+    HardwareProfile hp = builtin_profile(profile);
+    ModelPreset mp = model_preset(model);
+    BaselineMode m = baseline_mode_from_string(mode);
+    SplitPlan plan = make_split_plan(T, hp, mp.policy);
+    if (m == BaselineMode::TokenWeave && plan.mode != SplitMode::Overlap) m = BaselineMode::FuseOnly;
+    std::vector<StreamEvent> g = build_layer_graph(plan, mp.spec, hp, m, 0);
+    *seconds = simulate(g, hp).iteration_latency;
+  });
+}
+
+// --- CPU-baseline timers (the reference path as shipped, incl. its validation).
+
+// Times fused_allreduce_rmsnorm on a fixed group `iters` times; returns the
+// median milliseconds.  Residual shards are restored (outside the timed
+// region) before every call so each call sees the same inputs.
+int ref_time_fused(int world, std::int64_t T, std::int64_t H, int parallel, int iters,
+                   double* median_ms) {
+  return guarded([&] {
+    RankGroup g;
+    g.world_size = world;
+    std::mt19937_64 rng(1234);
+    std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+    for (int r = 0; r < world; ++r) {
+      TokenMatrix m = TokenMatrix::zeros(T, H);
+      for (float& v : m.values) v = dist(rng);
+      g.inputs.push_back(std::move(m));
+    }
+    const ShardMap shards = token_shard_map(T, world);
+    for (const TokenRange& range : shards.ranges) {
+      TokenMatrix m = TokenMatrix::zeros(range.size(), H);
+      for (float& v : m.values) v = dist(rng);
+      g.residual_shards.push_back(std::move(m));
+    }
+    NormParams p;
+    p.weight.assign(H, 1.0f);
+    const std::vector<TokenMatrix> saved = g.residual_shards;
+    std::vector<double> ms;
+    for (int i = 0; i < iters; ++i) {
+      g.residual_shards = saved;
+      const auto t0 = std::chrono::steady_clock::now();
+      TokenMatrix out = fused_allreduce_rmsnorm(g, p, shards, parallel != 0);
+      const auto t1 = std::chrono::steady_clock::now();
+      ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+    }
+    std::sort(ms.begin(), ms.end());
+    *median_ms = ms[ms.size() / 2];
+  });
+}
+
+// Times rmsnorm_residual over T x H with `threads` host threads, each calling
+// the reference rmsnorm_residual on a contiguous token chunk (the reference
+// op is single-threaded; chunking across cores is the caller-level
+// parallelism a host deployment would use).  Returns median milliseconds.
+int ref_time_rmsnorm(std::int64_t T, std::int64_t H, int threads, int iters, double* median_ms) {
+  return guarded([&] {
+    if (threads < 1) threads = 1;
+    std::mt19937_64 rng(4321);
+    std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+    std::vector<TokenMatrix> ins, ress;
+    const std::int64_t chunk = (T + threads - 1) / threads;
+    for (int c = 0; c < threads; ++c) {
+      const std::int64_t rows = std::max<std::int64_t>(0, std::min(T, (c + 1) * chunk) - c * chunk);
+      TokenMatrix a = TokenMatrix::zeros(rows, H), b = TokenMatrix::zeros(rows, H);
+      for (float& v : a.values) v = dist(rng);
+      for (float& v : b.values) v = dist(rng);
+      ins.push_back(std::move(a));
+      ress.push_back(std::move(b));
+    }
+    NormParams p;
+    p.weight.assign(H, 1.0f);
+    std::vector<double> ms;
+    for (int i = 0; i < iters; ++i) {
+      const auto t0 = std::chrono::steady_clock::now();
+      std::vector<std::thread> pool;
+      for (int c = 0; c < threads; ++c) {
+        pool.emplace_back([&, c] { NormResult r = rmsnorm_residual(ins[c], ress[c], p); (void)r; });
+      }
+      for (auto& th : pool) th.join();
+      const auto t1 = std::chrono::steady_clock::now();
+      ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+    }
+    std::sort(ms.begin(), ms.end());
+    *median_ms = ms[ms.size() / 2];
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,594 @@
+// tw_capi.cu -- the C-ABI (include/tw/tw.h): argument validation with the
+// reference's error taxonomy, the communicator (NVLS multicast objects or
+// peer buffers, signal pads), and dispatch to the row engine.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../kernels/tw_launch.h"
+#include "tw_internal.h"
+
+namespace tw {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void clear_error() { g_last_error.clear(); }
+
+tw_status fail(tw_status code, const std::string& msg) {
+  set_error(msg);
+  return code;
+}
+
+tw_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(TW_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+static void resolve(F*& fn, const char* name, bool& ok) {
+  cudaDriverEntryPointQueryResult q;
+  void* p = nullptr;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !p) {
+    ok = false;
+    return;
+  }
+  fn = reinterpret_cast<F*>(p);
+}
+
+const Driver& driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    bool ok = true;
+    resolve(d.getAttr, "cuDeviceGetAttribute", ok);
+    resolve(d.mcCreate, "cuMulticastCreate", ok);
+    resolve(d.mcGranularity, "cuMulticastGetGranularity", ok);
+    resolve(d.mcAddDevice, "cuMulticastAddDevice", ok);
+    resolve(d.mcBindMem, "cuMulticastBindMem", ok);
+    resolve(d.mcUnbind, "cuMulticastUnbind", ok);
+    resolve(d.memCreate, "cuMemCreate", ok);
+    resolve(d.memRelease, "cuMemRelease", ok);
+    resolve(d.memGranularity, "cuMemGetAllocationGranularity", ok);
+    resolve(d.addrReserve, "cuMemAddressReserve", ok);
+    resolve(d.addrFree, "cuMemAddressFree", ok);
+    resolve(d.memMap, "cuMemMap", ok);
+    resolve(d.memUnmap, "cuMemUnmap", ok);
+    resolve(d.memSetAccess, "cuMemSetAccess", ok);
+    resolve(d.getErrorString, "cuGetErrorString", ok);
+    d.ok = ok;
+  });
+  return d;
+}
+
+static std::string cu_str(CUresult r) {
+  const char* s = nullptr;
+  if (driver().getErrorString) driver().getErrorString(r, &s);
+  return s ? s : ("CUresult " + std::to_string(static_cast<int>(r)));
+}
+
+static int sm_count(int device) {
+  static int cache[64] = {0};
+  if (device < 0 || device >= 64) return 148;
+  if (!cache[device]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || n <= 0) n = 148;
+    cache[device] = n;
+  }
+  return cache[device];
+}
+
+static size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() { cudaGetDevice(&prev); }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// ---- communicator ------------------------------------------------------------------
+
+static tw_status create_peer(tw_comm* c) {
+  c->region = round_up(std::max<size_t>(c->bytes, 1), 256);
+  c->total = 3 * c->region + 4096;
+  for (int r = 0; r < c->world; ++r) {
+    RankBuffers& rb = c->ranks[r];
+    cudaError_t e = cudaSetDevice(rb.device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    char* base = nullptr;
+    e = cudaMalloc(&base, c->total);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(comm buffers)");
+    rb.owns_cuda_malloc = true;
+    for (int b = 0; b < 3; ++b) rb.buf[b] = base + b * c->region;
+    rb.pad = reinterpret_cast<uint32_t*>(base + 3 * c->region);
+    rb.err = reinterpret_cast<int*>(base + 3 * c->region + 2048);
+    e = cudaMemset(base + 3 * c->region, 0, 4096);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(pads)");
+  }
+  if (!c->colocated) {
+    for (int a = 0; a < c->world; ++a) {
+      cudaSetDevice(c->ranks[a].device);
+      for (int b = 0; b < c->world; ++b) {
+        const int da = c->ranks[a].device, db = c->ranks[b].device;
+        if (da == db) continue;
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, da, db);
+        if (!can) return fail(TW_ERR_UNSUPPORTED, "PEER transport: device " + std::to_string(da) +
+                                                      " cannot access device " + std::to_string(db));
+        cudaError_t e = cudaDeviceEnablePeerAccess(db, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) {
+          cudaGetLastError();
+        } else if (e != cudaSuccess) {
+          return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+        }
+      }
+    }
+  }
+  return TW_OK;
+}
+
+static tw_status create_nvls(tw_comm* c) {
+  const Driver& d = driver();
+  if (!d.ok) return fail(TW_ERR_UNSUPPORTED, "NVLS: driver multicast entry points unavailable");
+  for (const RankBuffers& rb : c->ranks) {
+    int mc = 0;
+    if (d.getAttr(&mc, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, rb.device) != CUDA_SUCCESS || !mc)
+      return fail(TW_ERR_UNSUPPORTED, "NVLS: device " + std::to_string(rb.device) + " lacks multicast support");
+  }
+  CUmulticastObjectProp mprop = {};
+  mprop.numDevices = static_cast<unsigned>(c->world);
+  mprop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  mprop.size = 1;
+  size_t mgran = 0;
+  CUresult r = d.mcGranularity(&mgran, &mprop, CU_MULTICAST_GRANULARITY_RECOMMENDED);
+  if (r != CUDA_SUCCESS) return fail(TW_ERR_UNSUPPORTED, "cuMulticastGetGranularity: " + cu_str(r));
+  CUmemAllocationProp aprop = {};
+  aprop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  aprop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  aprop.location.id = c->ranks[0].device;
+  aprop.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  size_t agran = 0;
+  r = d.memGranularity(&agran, &aprop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED);
+  if (r != CUDA_SUCCESS) return fail(TW_ERR_UNSUPPORTED, "cuMemGetAllocationGranularity: " + cu_str(r));
+  const size_t gran = std::max(mgran, agran);
+  c->region = round_up(std::max<size_t>(c->bytes, 1), gran);
+  c->total = 3 * c->region + gran;  // + one granule of signal pads
+  mprop.size = c->total;
+  r = d.mcCreate(&c->mc, &mprop);
+  if (r != CUDA_SUCCESS) return fail(TW_ERR_UNSUPPORTED, "cuMulticastCreate: " + cu_str(r));
+  for (const RankBuffers& rb : c->ranks) {
+    r = d.mcAddDevice(c->mc, rb.device);
+    if (r != CUDA_SUCCESS) return fail(TW_ERR_UNSUPPORTED, "cuMulticastAddDevice: " + cu_str(r));
+  }
+  for (RankBuffers& rb : c->ranks) {
+    cudaSetDevice(rb.device);
+    aprop.location.id = rb.device;
+    r = d.memCreate(&rb.phys, c->total, &aprop, 0);
+    if (r != CUDA_SUCCESS) return fail(TW_ERR_CUDA, "cuMemCreate: " + cu_str(r));
+    r = d.mcBindMem(c->mc, 0, rb.phys, 0, c->total, 0);
+    if (r != CUDA_SUCCESS) return fail(TW_ERR_UNSUPPORTED, "cuMulticastBindMem: " + cu_str(r));
+    CUmemAccessDesc acc = {};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = rb.device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    r = d.addrReserve(&rb.uc_base, c->total, gran, 0, 0);
+    if (r == CUDA_SUCCESS) r = d.memMap(rb.uc_base, c->total, 0, rb.phys, 0);
+    if (r == CUDA_SUCCESS) r = d.memSetAccess(rb.uc_base, c->total, &acc, 1);
+    if (r != CUDA_SUCCESS) return fail(TW_ERR_CUDA, "unicast map: " + cu_str(r));
+    r = d.addrReserve(&rb.mc_base, c->total, gran, 0, 0);
+    if (r == CUDA_SUCCESS) r = d.memMap(rb.mc_base, c->total, 0, c->mc, 0);
+    if (r == CUDA_SUCCESS) r = d.memSetAccess(rb.mc_base, c->total, &acc, 1);
+    if (r != CUDA_SUCCESS) return fail(TW_ERR_CUDA, "multicast map: " + cu_str(r));
+    char* uc = reinterpret_cast<char*>(rb.uc_base);
+    char* mcp = reinterpret_cast<char*>(rb.mc_base);
+    for (int b = 0; b < 3; ++b) {
+      rb.buf[b] = uc + b * c->region;
+      rb.mc_buf[b] = mcp + b * c->region;
+    }
+    rb.pad = reinterpret_cast<uint32_t*>(uc + 3 * c->region);
+    rb.mc_pad = reinterpret_cast<uint32_t*>(mcp + 3 * c->region);
+    rb.err = reinterpret_cast<int*>(uc + 3 * c->region + 2048);
+    cudaError_t e = cudaMemset(uc + 3 * c->region, 0, 4096);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(pads)");
+  }
+  for (RankBuffers& rb : c->ranks) {
+    cudaSetDevice(rb.device);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceSynchronize(comm create)");
+  }
+  return TW_OK;
+}
+
+static void destroy_comm(tw_comm* c) {
+  const Driver& d = driver();
+  for (RankBuffers& rb : c->ranks) {
+    cudaSetDevice(rb.device);
+    cudaDeviceSynchronize();
+    if (rb.owns_cuda_malloc && rb.buf[0]) cudaFree(rb.buf[0]);
+    if (rb.uc_base) {
+      d.memUnmap(rb.uc_base, c->total);
+      d.addrFree(rb.uc_base, c->total);
+    }
+    if (rb.mc_base) {
+      d.memUnmap(rb.mc_base, c->total);
+      d.addrFree(rb.mc_base, c->total);
+    }
+    if (c->mc && rb.phys) d.mcUnbind(c->mc, rb.device, 0, c->total);
+    if (rb.phys) d.memRelease(rb.phys);
+  }
+  if (c->mc) d.memRelease(c->mc);
+  delete c;
+}
+
+// ---- shared launch preparation --------------------------------------------------------
+
+struct Prep {
+  RowPlan plan;
+  bool bf16;
+  Xport x;
+  int budget;
+};
+
+}  // namespace tw
+
+using namespace tw;
+
+extern "C" {
+
+int tw_abi_version(void) { return TW_ABI_VERSION; }
+const char* tw_version(void) { return "tokenweave-b200 0.1 (sm_100a)"; }
+const char* tw_last_error(void) { return g_last_error.c_str(); }
+
+int tw_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+tw_status tw_token_shard_map(int64_t num_tokens, int world, int64_t* ranges) {
+  clear_error();
+  // proj/src/collectives.cpp:26-39
+  if (world < 2) return fail(TW_ERR_CONFIG, "token_shard_map: world_size must be >= 2");
+  if (num_tokens < 0) return fail(TW_ERR_DIMENSION, "token_shard_map: negative token count");
+  if (!ranges) return fail(TW_ERR_DIMENSION, "token_shard_map: null output");
+  const int64_t base = num_tokens / world, extra = num_tokens % world;
+  int64_t cursor = 0;
+  for (int r = 0; r < world; ++r) {
+    const int64_t len = base + (r < extra ? 1 : 0);
+    ranges[2 * r] = cursor;
+    ranges[2 * r + 1] = cursor + len;
+    cursor += len;
+  }
+  return TW_OK;
+}
+
+tw_status tw_shard_map_validate(const int64_t* ranges, int world, int64_t total_tokens) {
+  clear_error();
+  // proj/src/collectives.cpp:14-24
+  if (world < 1 || !ranges) return fail(TW_ERR_CONTRACT, "ShardMap: no ranges");
+  int64_t cursor = 0;
+  for (int r = 0; r < world; ++r) {
+    if (ranges[2 * r] != cursor || ranges[2 * r + 1] < ranges[2 * r])
+      return fail(TW_ERR_CONTRACT, "ShardMap: ranges must be contiguous, ascending, disjoint");
+    cursor = ranges[2 * r + 1];
+  }
+  if (cursor != total_tokens) return fail(TW_ERR_CONTRACT, "ShardMap: ranges must cover [0, T)");
+  return TW_OK;
+}
+
+tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* residual_out, void* output,
+                              const float* weight, int64_t T, int64_t H, float eps, tw_dtype dtype, int sm_budget,
+                              void* stream) {
+  clear_error();
+  // proj/src/numerics.cpp:18-45 (shape, weight, epsilon)
+  if (T < 0 || H < 1) return fail(TW_ERR_DIMENSION, "rmsnorm_residual: requires T >= 0 and H >= 1");
+  if (!(eps > 0.0f) && eps != 0.0f) return fail(TW_ERR_NUMERIC, "rmsnorm_residual: epsilon must be nonnegative");
+  if (dtype != TW_BF16 && dtype != TW_F32) return fail(TW_ERR_CONFIG, "rmsnorm_residual: unknown dtype");
+  if (T == 0) return TW_OK;
+  if (!input || !residual || !residual_out || !output || !weight)
+    return fail(TW_ERR_DIMENSION, "rmsnorm_residual: null buffer");
+  const bool bf16 = dtype == TW_BF16;
+  const int nv = bf16 ? 8 : 4;
+  const bool vec = H % nv == 0 && aligned16(input) && aligned16(residual) && aligned16(residual_out) &&
+                   aligned16(output) && aligned16(weight);
+  RowPlan plan;
+  if (!plan_rows(H, vec ? nv : 1, 256, &plan))
+    return fail(TW_ERR_DIMENSION, "rmsnorm_residual: hidden size too large for the row engine");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int bpsm = std::max(1, rownorm_blocks_per_sm(plan, bf16, Xport::Local));
+  const int sms = sm_budget > 0 ? std::min(sm_budget, sm_count(dev)) : sm_count(dev);
+  const long long need = (T + plan.groups - 1) / plan.groups;
+  const int grid = static_cast<int>(std::min<long long>(need, static_cast<long long>(sms) * bpsm));
+  RowParams p = {};
+  p.T = T;
+  p.H = H;
+  p.eps = eps;
+  p.in = input;
+  p.res_in = residual;
+  p.res_out = residual_out;
+  p.out = output;
+  p.weight = weight;
+  cudaError_t e = launch_rownorm(p, plan, bf16, Xport::Local, dim3(grid), static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "rmsnorm_residual launch");
+  return TW_OK;
+}
+
+tw_status tw_count_nonfinite(const void* x, int64_t n, tw_dtype dtype, int* count_dev, void* stream) {
+  clear_error();
+  if (n < 0) return fail(TW_ERR_DIMENSION, "count_nonfinite: negative size");
+  if (n > 0 && (!x || !count_dev)) return fail(TW_ERR_DIMENSION, "count_nonfinite: null buffer");
+  cudaError_t e = launch_count_nonfinite(x, n, dtype == TW_BF16, count_dev, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "count_nonfinite launch");
+  return TW_OK;
+}
+
+tw_status tw_comm_create(int world, const int* devices, size_t buffer_bytes, tw_transport transport, tw_comm_t* out) {
+  clear_error();
+  if (!out) return fail(TW_ERR_CONFIG, "comm_create: null output");
+  *out = nullptr;
+  if (world < 1 || world > kMaxRanks)
+    return fail(TW_ERR_CONFIG, "comm_create: world must be in [1, " + std::to_string(kMaxRanks) + "]");
+  if (!devices) return fail(TW_ERR_CONFIG, "comm_create: null device list");
+  const int ndev = tw_device_count();
+  if (ndev == 0) return fail(TW_ERR_CUDA, "comm_create: no CUDA device visible");
+  DeviceGuard guard;
+  tw_comm* c = new tw_comm();
+  c->world = world;
+  c->bytes = buffer_bytes;
+  c->ranks.resize(world);
+  bool distinct = true;
+  c->colocated = true;
+  for (int r = 0; r < world; ++r) {
+    if (devices[r] < 0 || devices[r] >= ndev) {
+      delete c;
+      return fail(TW_ERR_CONFIG, "comm_create: device " + std::to_string(devices[r]) + " out of range");
+    }
+    c->ranks[r].device = devices[r];
+    if (devices[r] != devices[0]) c->colocated = false;
+    for (int q = 0; q < r; ++q)
+      if (devices[q] == devices[r]) distinct = false;
+  }
+  if (!c->colocated && !distinct) {
+    delete c;
+    return fail(TW_ERR_CONFIG, "comm_create: ranks must be all on one device or all on distinct devices");
+  }
+  tw_status st;
+  if (transport == TW_TRANSPORT_NVLS || (transport == TW_TRANSPORT_AUTO && distinct && world >= 2)) {
+    c->transport = TW_TRANSPORT_NVLS;
+    if (!distinct || world < 2) {
+      delete c;
+      return fail(TW_ERR_UNSUPPORTED, "NVLS transport needs >= 2 ranks on distinct devices");
+    }
+    st = create_nvls(c);
+    if (st != TW_OK && transport == TW_TRANSPORT_AUTO) {
+      // AUTO: fall back to the PEER transport (still the GPU kernel path).
+      const std::string why = tw_last_error();
+      destroy_comm(c);
+      c = new tw_comm();
+      c->world = world;
+      c->bytes = buffer_bytes;
+      c->ranks.resize(world);
+      for (int r = 0; r < world; ++r) c->ranks[r].device = devices[r];
+      c->transport = TW_TRANSPORT_PEER;
+      st = create_peer(c);
+    }
+  } else {
+    c->transport = TW_TRANSPORT_PEER;
+    st = create_peer(c);
+  }
+  if (st != TW_OK) {
+    const std::string why = tw_last_error();
+    destroy_comm(c);
+    return fail(st, why);
+  }
+  *out = c;
+  return TW_OK;
+}
+
+tw_status tw_comm_destroy(tw_comm_t comm) {
+  clear_error();
+  if (!comm) return TW_OK;
+  DeviceGuard guard;
+  destroy_comm(comm);
+  return TW_OK;
+}
+
+tw_status tw_comm_info(tw_comm_t comm, int* world, tw_transport* transport, size_t* buffer_bytes) {
+  clear_error();
+  if (!comm) return fail(TW_ERR_CONFIG, "comm_info: null communicator");
+  if (world) *world = comm->world;
+  if (transport) *transport = comm->transport;
+  if (buffer_bytes) *buffer_bytes = comm->bytes;
+  return TW_OK;
+}
+
+tw_status tw_comm_buffer(tw_comm_t comm, int rank, tw_buffer which, void** device_ptr) {
+  clear_error();
+  if (!comm || !device_ptr) return fail(TW_ERR_CONFIG, "comm_buffer: null argument");
+  if (rank < 0 || rank >= comm->world) return fail(TW_ERR_CONFIG, "comm_buffer: rank out of range");
+  if (which < TW_BUF_INPUT || which > TW_BUF_RESIDUAL) return fail(TW_ERR_CONFIG, "comm_buffer: bad buffer id");
+  *device_ptr = comm->ranks[rank].buf[which];
+  return TW_OK;
+}
+
+tw_status tw_comm_multicast_buffer(tw_comm_t comm, int rank, tw_buffer which, void** device_ptr) {
+  clear_error();
+  if (!comm || !device_ptr) return fail(TW_ERR_CONFIG, "comm_multicast_buffer: null argument");
+  if (comm->transport != TW_TRANSPORT_NVLS) return fail(TW_ERR_UNSUPPORTED, "communicator is not NVLS");
+  if (rank < 0 || rank >= comm->world) return fail(TW_ERR_CONFIG, "comm_multicast_buffer: rank out of range");
+  if (which < TW_BUF_INPUT || which > TW_BUF_RESIDUAL) return fail(TW_ERR_CONFIG, "bad buffer id");
+  *device_ptr = comm->ranks[rank].mc_buf[which];
+  return TW_OK;
+}
+
+tw_status tw_comm_check(tw_comm_t comm) {
+  clear_error();
+  if (!comm) return fail(TW_ERR_CONFIG, "comm_check: null communicator");
+  DeviceGuard guard;
+  bool timed_out = false;
+  for (const RankBuffers& rb : comm->ranks) {
+    cudaSetDevice(rb.device);
+    int flag = 0;
+    cudaError_t e = cudaMemcpy(&flag, rb.err, sizeof(int), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "comm_check");
+    if (flag) {
+      timed_out = true;
+      cudaMemset(rb.err, 0, sizeof(int));
+    }
+  }
+  if (timed_out) return fail(TW_ERR_TIMEOUT, "cross-rank barrier timed out (a rank was not launched?)");
+  return TW_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Common validation + launch for the fused op (K1) and the AR baseline (K3).
+tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, const int64_t* shard_ranges, void* const* residual_shards,
+                      const float* const* weights, float eps, tw_dtype dtype, int sm_budget, unsigned flags,
+                      void* const* streams, bool fused) {
+  const char* op = fused ? "fused_allreduce_rmsnorm" : "allreduce";
+  if (!comm) return fail(TW_ERR_CONFIG, std::string(op) + ": null communicator");
+  const int W = comm->world;
+  if (W < 2) return fail(TW_ERR_CONFIG, std::string(op) + ": world_size must be >= 2");
+  if (T < 0 || H < 1) return fail(TW_ERR_DIMENSION, std::string(op) + ": requires T >= 0 and H >= 1");
+  if (dtype != TW_BF16 && dtype != TW_F32) return fail(TW_ERR_CONFIG, std::string(op) + ": unknown dtype");
+  const bool bf16 = dtype == TW_BF16;
+  const size_t esz = bf16 ? 2 : 4;
+  if (static_cast<size_t>(T) * static_cast<size_t>(H) * esz > comm->bytes)
+    return fail(TW_ERR_DIMENSION, std::string(op) + ": T*H exceeds the communicator buffer size");
+  int64_t local_ranges[2 * kMaxRanks];
+  if (!shard_ranges) {
+    tw_token_shard_map(T, W, local_ranges);
+    shard_ranges = local_ranges;
+  }
+  tw_status st = tw_shard_map_validate(shard_ranges, W, T);
+  if (st != TW_OK) return st;
+  if (fused) {
+    if (!(eps > 0.0f) && eps != 0.0f) return fail(TW_ERR_NUMERIC, "fused_allreduce_rmsnorm: epsilon must be nonnegative");
+    if (!weights) return fail(TW_ERR_DIMENSION, "fused_allreduce_rmsnorm: null weight list");
+    if (!residual_shards) return fail(TW_ERR_DIMENSION, "fused_allreduce_rmsnorm: null residual list");
+    for (int r = 0; r < W; ++r) {
+      if (!weights[r]) return fail(TW_ERR_DIMENSION, "fused_allreduce_rmsnorm: null weight");
+      if (shard_ranges[2 * r + 1] > shard_ranges[2 * r] && !residual_shards[r])
+        return fail(TW_ERR_DIMENSION, "fused_allreduce_rmsnorm: null residual shard");
+    }
+  }
+  if (T == 0) return TW_OK;
+  const bool nvls = comm->transport == TW_TRANSPORT_NVLS;
+  const int nv = bf16 ? 8 : 4;
+  bool vec = H % nv == 0;
+  if (fused) {
+    for (int r = 0; r < W && vec; ++r) {
+      vec = aligned16(weights[r]) && (residual_shards[r] == nullptr || aligned16(residual_shards[r]));
+    }
+  }
+  if (nvls && !vec)
+    return fail(TW_ERR_UNSUPPORTED, std::string(op) + ": NVLS transport needs H % " + std::to_string(nv) +
+                                        " == 0 and 16-byte aligned buffers");
+  RowPlan plan;
+  if (!plan_rows(H, vec ? nv : 1, nvls ? 128 : 256, &plan))
+    return fail(TW_ERR_DIMENSION, std::string(op) + ": hidden size too large for the row engine");
+  const Xport x = nvls ? Xport::Nvls : Xport::Peer;
+
+  DeviceGuard guard;
+  int budget = sm_budget > 0 ? sm_budget : 8;
+  const int dev0 = comm->ranks[0].device;
+  cudaSetDevice(dev0);
+  const int sms = sm_count(dev0);
+  if (fused) {
+    const int bpsm = std::max(1, rownorm_blocks_per_sm(plan, bf16, x));
+    const int slots = comm->colocated ? W : 1;
+    // Every CTA of every co-launched rank must be resident for the barrier.
+    budget = std::min(budget, std::max(1, sms * bpsm / slots));
+  } else {
+    budget = std::min(budget, std::max(1, sms / (comm->colocated ? W : 1)));
+  }
+  const uint32_t per_barrier = static_cast<uint32_t>(W) * static_cast<uint32_t>(budget);
+  RowParams p = {};
+  p.T = T;
+  p.H = H;
+  p.eps = eps;
+  p.flags = flags;
+  p.world = W;
+  p.entry_target = static_cast<uint32_t>(comm->arrivals + per_barrier);
+  p.exit_target = static_cast<uint32_t>(comm->arrivals + 2ull * per_barrier);
+  for (int q = 0; q < W; ++q) {
+    p.peer_in[q] = comm->ranks[q].buf[TW_BUF_INPUT];
+    p.peer_out[q] = comm->ranks[q].buf[TW_BUF_OUTPUT];
+    p.peer_res[q] = comm->ranks[q].buf[TW_BUF_RESIDUAL];
+    p.peer_pad[q] = comm->ranks[q].pad;
+  }
+  auto fill_slot = [&](RankSlot& s, int r) {
+    s.rank = r;
+    s.begin = shard_ranges[2 * r];
+    s.end = shard_ranges[2 * r + 1];
+    s.residual = fused ? residual_shards[r] : nullptr;
+    s.weight = fused ? weights[r] : nullptr;
+    s.pad = comm->ranks[r].pad;
+  };
+  auto launch = [&](const RowParams& pp, dim3 grid, cudaStream_t s) {
+    return fused ? launch_rownorm(pp, plan, bf16, x, grid, s) : launch_allreduce(pp, plan, bf16, x, grid, s);
+  };
+  if (comm->colocated) {
+    p.nslots = W;
+    for (int r = 0; r < W; ++r) fill_slot(p.slot[r], r);
+    p.err = comm->ranks[0].err;
+    cudaStream_t s = streams ? static_cast<cudaStream_t>(streams[0]) : nullptr;
+    cudaError_t e = launch(p, dim3(budget, W), s);
+    if (e != cudaSuccess) return cuda_fail(e, op);
+  } else {
+    for (int r = 0; r < W; ++r) {
+      cudaSetDevice(comm->ranks[r].device);
+      RowParams pr = p;
+      pr.nslots = 1;
+      fill_slot(pr.slot[0], r);
+      pr.err = comm->ranks[r].err;
+      if (nvls) {
+        pr.mc_in = comm->ranks[r].mc_buf[TW_BUF_INPUT];
+        pr.mc_out = comm->ranks[r].mc_buf[TW_BUF_OUTPUT];
+        pr.mc_res = comm->ranks[r].mc_buf[TW_BUF_RESIDUAL];
+        pr.mc_pad = comm->ranks[r].mc_pad;
+      }
+      cudaStream_t s = streams ? static_cast<cudaStream_t>(streams[r]) : nullptr;
+      cudaError_t e = launch(pr, dim3(budget, 1), s);
+      if (e != cudaSuccess) return cuda_fail(e, op);
+    }
+  }
+  comm->arrivals += 2ull * per_barrier;
+  return TW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tw_status tw_fused_allreduce_rmsnorm_group(tw_comm_t comm, int64_t T, int64_t H, const int64_t* shard_ranges,
+                                           void* const* residual_shards, const float* const* weights, float eps,
+                                           tw_dtype dtype, int sm_budget, unsigned flags, void* const* streams) {
+  clear_error();
+  return comm_launch(comm, T, H, shard_ranges, residual_shards, weights, eps, dtype, sm_budget, flags, streams, true);
+}
+
+tw_status tw_allreduce_group(tw_comm_t comm, int64_t T, int64_t H, tw_dtype dtype, int sm_budget, void* const* streams) {
+  clear_error();
+  return comm_launch(comm, T, H, nullptr, nullptr, nullptr, 0.0f, dtype, sm_budget, 0u, streams, false);
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+// tw_internal.h -- host-side internals of libtw.so (communicator, errors).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "tw/tw.h"
+
+namespace tw {
+
+// Thread-local last-error message behind tw_last_error().
+void set_error(const std::string& msg);
+void clear_error();
+tw_status fail(tw_status code, const std::string& msg);
+tw_status cuda_fail(cudaError_t e, const char* what);
+
+// Driver API entry points resolved through cudaGetDriverEntryPoint, so the
+// library has no link-time dependency on libcuda (it loads on GPU-less hosts).
+struct Driver {
+  bool ok = false;
+  CUresult (*getAttr)(int*, CUdevice_attribute, CUdevice) = nullptr;
+  CUresult (*mcCreate)(CUmemGenericAllocationHandle*, const CUmulticastObjectProp*) = nullptr;
+  CUresult (*mcGranularity)(size_t*, const CUmulticastObjectProp*, CUmulticastGranularity_flags) = nullptr;
+  CUresult (*mcAddDevice)(CUmemGenericAllocationHandle, CUdevice) = nullptr;
+  CUresult (*mcBindMem)(CUmemGenericAllocationHandle, size_t, CUmemGenericAllocationHandle, size_t, size_t,
+                        unsigned long long) = nullptr;
+  CUresult (*mcUnbind)(CUmemGenericAllocationHandle, CUdevice, size_t, size_t) = nullptr;
+  CUresult (*memCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) =
+      nullptr;
+  CUresult (*memRelease)(CUmemGenericAllocationHandle) = nullptr;
+  CUresult (*memGranularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+  CUresult (*addrReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+  CUresult (*addrFree)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*memMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+  CUresult (*memUnmap)(CUdeviceptr, size_t) = nullptr;
+  CUresult (*memSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+  CUresult (*getErrorString)(CUresult, const char**) = nullptr;
+};
+const Driver& driver();
+
+struct RankBuffers {
+  int device = 0;
+  void* buf[3] = {nullptr, nullptr, nullptr};  // INPUT, OUTPUT, RESIDUAL (unicast)
+  uint32_t* pad = nullptr;                      // signal pad (unicast)
+  int* err = nullptr;                           // barrier-timeout flag
+  // NVLS
+  void* mc_buf[3] = {nullptr, nullptr, nullptr};
+  uint32_t* mc_pad = nullptr;
+  CUmemGenericAllocationHandle phys = 0;
+  CUdeviceptr uc_base = 0, mc_base = 0;
+  bool owns_cuda_malloc = false;
+};
+
+}  // namespace tw
+
+struct tw_comm {
+  int world = 0;
+  tw_transport transport = TW_TRANSPORT_PEER;
+  size_t bytes = 0;         // per symmetric buffer
+  size_t region = 0;        // aligned per-buffer stride inside one allocation
+  size_t total = 0;         // bytes of one rank's allocation
+  bool colocated = false;   // every rank on the same device
+  std::vector<tw::RankBuffers> ranks;
+  CUmemGenericAllocationHandle mc = 0;
+  uint64_t arrivals = 0;    // cumulative signal-pad arrivals per rank (host mirror)
+};

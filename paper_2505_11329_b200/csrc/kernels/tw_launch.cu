@@ -1,0 +1,171 @@
+// tw_launch.cu -- instantiation and launch of the row engine (K1, K2) and of
+// the unfused AllReduce baseline kernel (K3).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "tw_launch.h"
+#include "tw_rownorm.cuh"
+
+namespace tw {
+
+// ---- K3: one-shot AllReduce baseline (collectives.cpp:82-88 semantics) --------
+// Rank r reduces its token shard and broadcasts it: OUTPUT[t] = sum_q INPUT_q[t].
+template <class E, int N, Xport X>
+__global__ void __launch_bounds__(kBlock, 1) allreduce_kernel(const __grid_constant__ RowParams p) {
+  using VT = Vec<E, N>;
+  const RankSlot& s = p.slot[blockIdx.y];
+  rank_barrier<X>(p, s, p.entry_target);
+  const long long n = (s.end - s.begin) * p.V;  // vectors in the shard
+  const long long base = s.begin * p.H;
+  for (long long v = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
+       v += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long e = base + v * N;
+    if constexpr (X == Xport::Nvls) {
+      VT::mm_store(p.mc_out, e, VT::mm_reduce(p.mc_in, e));
+    } else {
+      float acc[N];
+#pragma unroll
+      for (int i = 0; i < N; ++i) acc[i] = 0.0f;
+      for (int q = 0; q < p.world; ++q) {
+        float f[N];
+        VT::unpack(VT::load(p.peer_in[q], e), f);
+#pragma unroll
+        for (int i = 0; i < N; ++i) acc[i] += f[i];
+      }
+      const auto packed = VT::pack(acc);
+      for (int q = 0; q < p.world; ++q) VT::store(p.peer_out[q], e, packed);
+    }
+  }
+  rank_barrier<X>(p, s, p.exit_target);
+}
+
+namespace {
+
+using KernelFn = void (*)(RowParams);
+
+template <class E, int N, Xport X>
+KernelFn pick_rownorm(int vpt) {
+  switch (vpt) {
+    case 1: return rownorm_kernel<E, N, 1, X>;
+    case 2: return rownorm_kernel<E, N, 2, X>;
+    case 4: return rownorm_kernel<E, N, 4, X>;
+    case 8: return rownorm_kernel<E, N, 8, X>;
+    case 16: return rownorm_kernel<E, N, 16, X>;
+    default: return nullptr;
+  }
+}
+
+template <class E, int N>
+KernelFn pick_by_xport(Xport x, int vpt) {
+  switch (x) {
+    case Xport::Local: return pick_rownorm<E, N, Xport::Local>(vpt);
+    case Xport::Peer: return pick_rownorm<E, N, Xport::Peer>(vpt);
+    case Xport::Nvls:
+      if constexpr (N > 1) return pick_rownorm<E, N, Xport::Nvls>(vpt);
+      return nullptr;
+  }
+  return nullptr;
+}
+
+KernelFn pick_kernel(bool bf16, int N, Xport x, int vpt) {
+  if (bf16) return N == 8 ? pick_by_xport<uint16_t, 8>(x, vpt) : pick_by_xport<uint16_t, 1>(x, vpt);
+  return N == 4 ? pick_by_xport<float, 4>(x, vpt) : pick_by_xport<float, 1>(x, vpt);
+}
+
+KernelFn pick_allreduce(bool bf16, int N, Xport x) {
+  if (x == Xport::Nvls) {
+    if (bf16 && N == 8) return allreduce_kernel<uint16_t, 8, Xport::Nvls>;
+    if (!bf16 && N == 4) return allreduce_kernel<float, 4, Xport::Nvls>;
+    return nullptr;
+  }
+  if (bf16) return N == 8 ? allreduce_kernel<uint16_t, 8, Xport::Peer> : allreduce_kernel<uint16_t, 1, Xport::Peer>;
+  return N == 4 ? allreduce_kernel<float, 4, Xport::Peer> : allreduce_kernel<float, 1, Xport::Peer>;
+}
+
+int round32(long long x) { return static_cast<int>(((x + 31) / 32) * 32); }
+
+}  // namespace
+
+bool plan_rows(long long H, int elems_per_vec, int tpr_pref, RowPlan* plan) {
+  if (H < 1 || H % elems_per_vec) return false;
+  const long long V = H / elems_per_vec;
+  const int vpts[] = {1, 2, 4, 8, 16};
+  for (int vpt : vpts) {
+    const int tpr = std::max(32, round32((V + vpt - 1) / vpt));
+    if (tpr <= tpr_pref || (vpt == 16 && tpr <= kBlock)) {
+      plan->N = elems_per_vec;
+      plan->V = static_cast<int>(V);
+      plan->vpt = vpt;
+      plan->tpr = tpr;
+      plan->groups = std::min(kMaxGroups, kBlock / tpr);
+      return true;
+    }
+  }
+  return false;
+}
+
+cudaError_t launch_rownorm(const RowParams& params, const RowPlan& plan, bool bf16, Xport x, dim3 grid,
+                           cudaStream_t stream) {
+  KernelFn fn = pick_kernel(bf16, plan.N, x, plan.vpt);
+  if (!fn) return cudaErrorInvalidConfiguration;
+  RowParams p = params;
+  p.V = plan.V;
+  p.tpr = plan.tpr;
+  void* args[] = {&p};
+  return cudaLaunchKernel(reinterpret_cast<const void*>(fn), grid, dim3(plan.groups * plan.tpr), args, 0, stream);
+}
+
+cudaError_t launch_allreduce(const RowParams& params, const RowPlan& plan, bool bf16, Xport x, dim3 grid,
+                             cudaStream_t stream) {
+  KernelFn fn = pick_allreduce(bf16, plan.N, x);
+  if (!fn) return cudaErrorInvalidConfiguration;
+  RowParams p = params;
+  p.V = plan.V;
+  p.tpr = plan.tpr;
+  void* args[] = {&p};
+  return cudaLaunchKernel(reinterpret_cast<const void*>(fn), grid, dim3(kBlock), args, 0, stream);
+}
+
+int rownorm_blocks_per_sm(const RowPlan& plan, bool bf16, Xport x) {
+  KernelFn fn = pick_kernel(bf16, plan.N, x, plan.vpt);
+  if (!fn) return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reinterpret_cast<const void*>(fn), plan.groups * plan.tpr,
+                                                    0) != cudaSuccess)
+    return 0;
+  return n;
+}
+
+// ---- finite scan (TokenMatrix::validate, numerics.cpp:25-27) ---------------------
+
+template <class E>
+__global__ void count_nonfinite_kernel(const E* x, long long n, int* count) {
+  int local = 0;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    float f;
+    if constexpr (sizeof(E) == 2) {
+      f = bf16_to_f32(x[i]);
+    } else {
+      f = x[i];
+    }
+    local += !isfinite(f);
+  }
+  local = __reduce_add_sync(0xffffffffu, local);
+  if ((threadIdx.x & 31) == 0 && local) atomicAdd(count, local);
+}
+
+cudaError_t launch_count_nonfinite(const void* x, long long n, bool bf16, int* count, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  const int block = 256;
+  const int grid = static_cast<int>(std::min<long long>((n + block - 1) / block, 148LL * 8));
+  if (bf16)
+    count_nonfinite_kernel<uint16_t><<<grid, block, 0, stream>>>(static_cast<const uint16_t*>(x), n, count);
+  else
+    count_nonfinite_kernel<float><<<grid, block, 0, stream>>>(static_cast<const float*>(x), n, count);
+  return cudaGetLastError();
+}
+
+}  // namespace tw

@@ -1,0 +1,30 @@
+// tw_launch.h -- host-side launch interface of the row engine (internal).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "tw_rownorm.cuh"
+
+namespace tw {
+
+struct RowPlan {
+  int N;       // elements per vector (8 bf16 / 4 f32 / 1 scalar)
+  int V;       // vectors per row
+  int vpt;     // vectors per thread
+  int tpr;     // threads per row group
+  int groups;  // row groups per CTA
+};
+
+// Chooses vectors-per-thread and threads-per-row for a row of H elements
+// loaded N at a time.  tpr_pref bounds the row-group width (fewer threads per
+// row = more rows in flight per CTA).  Returns false if H is unsupported.
+bool plan_rows(long long H, int elems_per_vec, int tpr_pref, RowPlan* plan);
+
+cudaError_t launch_rownorm(const RowParams& params, const RowPlan& plan, bool bf16, Xport x, dim3 grid,
+                           cudaStream_t stream);
+cudaError_t launch_allreduce(const RowParams& params, const RowPlan& plan, bool bf16, Xport x, dim3 grid,
+                             cudaStream_t stream);
+int rownorm_blocks_per_sm(const RowPlan& plan, bool bf16, Xport x);
+cudaError_t launch_count_nonfinite(const void* x, long long n, bool bf16, int* count, cudaStream_t stream);
+
+}  // namespace tw

@@ -1,0 +1,357 @@
+// tw_rownorm.cuh -- the row engine shared by K1 (fused AllReduce + residual +
+// RMSNorm) and K2 (TP=1 fused residual + RMSNorm).
+//
+// One "row group" of `tpr` threads owns one token row at a time; a CTA holds
+// blockDim/tpr groups, so several rows are in flight per SM.  Per row:
+//   x   = the reduced input row   (K2: local load; K1: NVLS multimem.ld_reduce
+//                                  or rank-ascending sum of peer loads)
+//   r'  = x + residual             (fp32; stored back rounded to the dtype)
+//   ss  = sum r'^2                 (fp32 for bf16, double for fp32 -- the
+//                                  reference's double accumulator,
+//                                  proj/src/numerics.cpp:51-56)
+//   out = r' * (1/sqrt(ss/H + eps)) * w    (proj/src/numerics.cpp:57-61)
+// The row reduction is warp shuffles + a double-buffered shared partial and
+// one named barrier per row (no __syncthreads on the row path).
+//
+// K1 brackets the row loop with the cross-rank signal-pad barrier
+// (PAPER.md:418,453): every CTA of every rank adds 1 to every rank's pad
+// (multimem.red on NVLS, red.release per peer otherwise) and waits on its own
+// pad with ld.acquire.sys for the host-tracked cumulative target.
+#pragma once
+
+#include <cstdint>
+#include <type_traits>
+
+#include "tw_ptx.cuh"
+
+namespace tw {
+
+enum class Xport : int { Local = 0, Peer = 1, Nvls = 2 };
+
+constexpr int kMaxRanks = 8;
+constexpr int kMaxGroups = 16;
+constexpr int kBlock = 512;  // threads per CTA upper bound (launch bounds)
+
+struct RankSlot {
+  int rank;
+  int pad_;
+  long long begin, end;  // owned token shard [begin, end)
+  void* residual;        // shard rows [end-begin, H], updated in place
+  const float* weight;   // fp32[H] on this device
+  uint32_t* pad;         // this rank's own signal pad (unicast VA)
+};
+
+struct RowParams {
+  long long T, H;
+  int V;    // vectors per row (H / N)
+  int tpr;  // threads per row group (multiple of 32)
+  float eps;
+  unsigned flags;
+  // K2 (Local)
+  const void* in;
+  const void* res_in;
+  void* res_out;
+  void* out;
+  const float* weight;
+  // K1
+  int world;
+  int nslots;
+  RankSlot slot[kMaxRanks];
+  void* peer_in[kMaxRanks];
+  void* peer_out[kMaxRanks];
+  void* peer_res[kMaxRanks];
+  uint32_t* peer_pad[kMaxRanks];
+  void* mc_in;
+  void* mc_out;
+  void* mc_res;
+  uint32_t* mc_pad;
+  uint32_t entry_target, exit_target;
+  int* err;
+  int skip_entry;  // 1: caller guarantees inputs are globally visible (tests)
+};
+
+constexpr unsigned kGatherResidual = 0x1u;
+
+// ---- typed vector access -------------------------------------------------------
+// N elements of E per "vector": 8 x bf16 or 4 x f32 (16 B), or 1 element.
+
+template <class E, int N>
+struct Vec;
+
+template <>
+struct Vec<uint16_t, 8> {  // bf16 x 8
+  using Raw = uint4;
+  static __device__ __forceinline__ Raw load(const void* base, long long e) {
+    return ld_v4(static_cast<const uint16_t*>(base) + e);
+  }
+  static __device__ __forceinline__ Raw load_stream(const void* base, long long e) {
+    return ld_stream_v4(static_cast<const uint16_t*>(base) + e);
+  }
+  static __device__ __forceinline__ Raw mm_reduce(const void* mc, long long e) {
+    return mm_ld_reduce_bf16x8(static_cast<const uint16_t*>(mc) + e);
+  }
+  static __device__ __forceinline__ void store(void* base, long long e, Raw v) {
+    st_v4(static_cast<uint16_t*>(base) + e, v);
+  }
+  static __device__ __forceinline__ void mm_store(void* mc, long long e, Raw v) {
+    mm_st_v4(static_cast<uint16_t*>(mc) + e, v);
+  }
+  static __device__ __forceinline__ void unpack(Raw v, float (&f)[8]) {
+    f[0] = bf16lo(v.x); f[1] = bf16hi(v.x); f[2] = bf16lo(v.y); f[3] = bf16hi(v.y);
+    f[4] = bf16lo(v.z); f[5] = bf16hi(v.z); f[6] = bf16lo(v.w); f[7] = bf16hi(v.w);
+  }
+  static __device__ __forceinline__ Raw pack(const float (&f)[8]) {
+    return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                      pack_bf16x2(f[6], f[7]));
+  }
+};
+
+template <>
+struct Vec<float, 4> {  // f32 x 4
+  using Raw = uint4;
+  static __device__ __forceinline__ Raw load(const void* base, long long e) {
+    return ld_v4(static_cast<const float*>(base) + e);
+  }
+  static __device__ __forceinline__ Raw load_stream(const void* base, long long e) {
+    return ld_stream_v4(static_cast<const float*>(base) + e);
+  }
+  static __device__ __forceinline__ Raw mm_reduce(const void* mc, long long e) {
+    return mm_ld_reduce_f32x4(static_cast<const float*>(mc) + e);
+  }
+  static __device__ __forceinline__ void store(void* base, long long e, Raw v) {
+    st_v4(static_cast<float*>(base) + e, v);
+  }
+  static __device__ __forceinline__ void mm_store(void* mc, long long e, Raw v) {
+    mm_st_v4(static_cast<float*>(mc) + e, v);
+  }
+  static __device__ __forceinline__ void unpack(Raw v, float (&f)[4]) {
+    f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
+    f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+  }
+  static __device__ __forceinline__ Raw pack(const float (&f)[4]) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                      __float_as_uint(f[3]));
+  }
+};
+
+template <>
+struct Vec<uint16_t, 1> {  // scalar bf16 (H not a multiple of 8)
+  using Raw = uint32_t;
+  static __device__ __forceinline__ Raw load(const void* base, long long e) {
+    return static_cast<const uint16_t*>(base)[e];
+  }
+  static __device__ __forceinline__ Raw load_stream(const void* base, long long e) { return load(base, e); }
+  static __device__ __forceinline__ Raw mm_reduce(const void*, long long) { __trap(); return 0; }
+  static __device__ __forceinline__ void store(void* base, long long e, Raw v) {
+    static_cast<uint16_t*>(base)[e] = static_cast<uint16_t>(v);
+  }
+  static __device__ __forceinline__ void mm_store(void*, long long, Raw) { __trap(); }
+  static __device__ __forceinline__ void unpack(Raw v, float (&f)[1]) { f[0] = __uint_as_float(v << 16); }
+  static __device__ __forceinline__ Raw pack(const float (&f)[1]) { return f32_to_bf16(f[0]); }
+};
+
+template <>
+struct Vec<float, 1> {  // scalar f32 (H not a multiple of 4)
+  using Raw = uint32_t;
+  static __device__ __forceinline__ Raw load(const void* base, long long e) {
+    return __float_as_uint(static_cast<const float*>(base)[e]);
+  }
+  static __device__ __forceinline__ Raw load_stream(const void* base, long long e) { return load(base, e); }
+  static __device__ __forceinline__ Raw mm_reduce(const void* mc, long long e) {
+    return __float_as_uint(mm_ld_reduce_f32(static_cast<const float*>(mc) + e));
+  }
+  static __device__ __forceinline__ void store(void* base, long long e, Raw v) {
+    static_cast<float*>(base)[e] = __uint_as_float(v);
+  }
+  static __device__ __forceinline__ void mm_store(void* mc, long long e, Raw v) {
+    mm_st_b32(static_cast<float*>(mc) + e, v);
+  }
+  static __device__ __forceinline__ void unpack(Raw v, float (&f)[1]) { f[0] = __uint_as_float(v); }
+  static __device__ __forceinline__ Raw pack(const float (&f)[1]) { return __float_as_uint(f[0]); }
+};
+
+template <int N>
+__device__ __forceinline__ void load_weight(const float* w, long long e, float (&f)[N]) {
+  if constexpr (N == 8) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(w + e));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(w + e) + 1);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  } else if constexpr (N == 4) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(w + e));
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+  } else {
+    f[0] = __ldg(w + e);
+  }
+}
+
+template <class Acc>
+__device__ __forceinline__ Acc warp_sum(Acc v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ---- cross-rank barrier ------------------------------------------------------------
+
+template <Xport X>
+__device__ __forceinline__ void rank_barrier(const RowParams& p, const RankSlot& s, uint32_t target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if constexpr (X == Xport::Nvls) {
+      mm_red_release_add(p.mc_pad, 1u);
+    } else {
+      for (int q = 0; q < p.world; ++q) red_release_add(p.peer_pad[q], 1u);
+    }
+    long long spins = 0;
+    while (static_cast<int>(ld_acquire(s.pad) - target) < 0) {
+      if (++spins > (1ll << 25)) {  // ~seconds: a rank was never launched
+        atomicExch(p.err, 1);
+        break;
+      }
+      __nanosleep(64);
+    }
+    if constexpr (X == Xport::Nvls) fence_proxy_alias();
+  }
+  __syncthreads();
+}
+
+// ---- the row kernel ------------------------------------------------------------------
+
+template <class E, int N, int VPT, Xport X>
+__global__ void __launch_bounds__(kBlock, 1) rownorm_kernel(const __grid_constant__ RowParams p) {
+  using VT = Vec<E, N>;
+  using Raw = typename VT::Raw;
+  // fp32 activations keep the reference's double sum of squares.
+  using Acc = typename std::conditional<sizeof(E) == 4, double, float>::type;
+  __shared__ Acc part[kMaxGroups][2][kBlock / 32];
+
+  const int slot_idx = (X == Xport::Local) ? 0 : static_cast<int>(blockIdx.y);
+  const RankSlot& s = p.slot[slot_idx];
+  const int tpr = p.tpr;
+  const int groups = blockDim.x / tpr;
+  const int group = threadIdx.x / tpr;
+  const int lt = threadIdx.x - group * tpr;
+  const int warp_in_group = lt >> 5;
+  const int nwarps = tpr >> 5;
+  const long long H = p.H;
+
+  if constexpr (X != Xport::Local) {
+    if (!p.skip_entry) rank_barrier<X>(p, s, p.entry_target);
+  }
+
+  long long row0, row1;
+  if constexpr (X == Xport::Local) {
+    row0 = 0;
+    row1 = p.T;
+  } else {
+    row0 = s.begin;
+    row1 = s.end;
+  }
+  const long long stride = static_cast<long long>(gridDim.x) * groups;
+  int parity = 0;
+  for (long long t = row0 + static_cast<long long>(blockIdx.x) * groups + group; t < row1;
+       t += stride, parity ^= 1) {
+    const long long rowe = t * H;  // element offset of the row in [T,H] buffers
+    const long long srow = (X == Xport::Local) ? rowe : (t - row0) * H;  // residual row
+    const void* res_src = (X == Xport::Local) ? p.res_in : s.residual;
+    void* res_dst = (X == Xport::Local) ? p.res_out : s.residual;
+
+    // Phase 1: issue every load of the row before using any of them.
+    Raw xr[VPT], rr[VPT];
+    float xs[(X == Xport::Peer) ? VPT : 1][N];  // Peer: fp32 rank-sum accumulators
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int c = lt + k * tpr;
+      if (c < p.V) {
+        const long long e = rowe + static_cast<long long>(c) * N;
+        if constexpr (X == Xport::Local) {
+          xr[k] = VT::load_stream(p.in, e);
+        } else if constexpr (X == Xport::Nvls) {
+          xr[k] = VT::mm_reduce(p.mc_in, e);
+        } else {
+          // Rank-ascending fp32 sum from 0.0f (proj/src/collectives.cpp:74-78).
+#pragma unroll
+          for (int i = 0; i < N; ++i) xs[k][i] = 0.0f;
+          for (int q = 0; q < p.world; ++q) {
+            float f[N];
+            VT::unpack(VT::load(p.peer_in[q], e), f);
+#pragma unroll
+            for (int i = 0; i < N; ++i) xs[k][i] += f[i];
+          }
+        }
+        rr[k] = VT::load_stream(res_src, srow + static_cast<long long>(c) * N);
+      }
+    }
+    // Phase 2: r' = x + res (fp32), rounded to the storage type and written
+    // back; the sum of squares is taken over the stored (rounded) r' so the
+    // output is exactly the RMSNorm of the residual the caller gets back.
+    Acc ss = 0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int c = lt + k * tpr;
+      if (c < p.V) {
+        float x[N], r[N];
+        if constexpr (X == Xport::Peer) {
+#pragma unroll
+          for (int i = 0; i < N; ++i) x[i] = xs[k][i];
+        } else {
+          VT::unpack(xr[k], x);
+        }
+        VT::unpack(rr[k], r);
+#pragma unroll
+        for (int i = 0; i < N; ++i) r[i] = x[i] + r[i];
+        rr[k] = VT::pack(r);
+        VT::unpack(rr[k], r);
+#pragma unroll
+        for (int i = 0; i < N; ++i) ss += static_cast<Acc>(r[i]) * static_cast<Acc>(r[i]);
+        VT::store(res_dst, srow + static_cast<long long>(c) * N, rr[k]);
+        if (p.flags & kGatherResidual) {
+          const long long e = rowe + static_cast<long long>(c) * N;
+          if constexpr (X == Xport::Nvls) {
+            VT::mm_store(p.mc_res, e, rr[k]);
+          } else if constexpr (X == Xport::Peer) {
+            for (int q = 0; q < p.world; ++q) VT::store(p.peer_res[q], e, rr[k]);
+          }
+        }
+      }
+    }
+    // Phase 3: row reduction.
+    ss = warp_sum(ss);
+    Acc total;
+    if (nwarps == 1) {
+      total = ss;
+    } else {
+      if ((lt & 31) == 0) part[group][parity][warp_in_group] = ss;
+      named_bar_sync(1 + group, tpr);
+      total = 0;
+      for (int w = 0; w < nwarps; ++w) total += part[group][parity][w];
+    }
+    const float inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(H)) + p.eps);
+    // Phase 4: out = r' * inv * w, stored locally / to every rank.
+    const float* wgt = (X == Xport::Local) ? p.weight : s.weight;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int c = lt + k * tpr;
+      if (c < p.V) {
+        const long long e = static_cast<long long>(c) * N;
+        float w[N], o[N];
+        load_weight<N>(wgt, e, w);
+        VT::unpack(rr[k], o);
+#pragma unroll
+        for (int i = 0; i < N; ++i) o[i] = o[i] * inv * w[i];
+        const Raw ov = VT::pack(o);
+        if constexpr (X == Xport::Local) {
+          VT::store(p.out, rowe + e, ov);
+        } else if constexpr (X == Xport::Nvls) {
+          VT::mm_store(p.mc_out, rowe + e, ov);
+        } else {
+          for (int q = 0; q < p.world; ++q) VT::store(p.peer_out[q], rowe + e, ov);
+        }
+      }
+    }
+  }
+
+  if constexpr (X != Xport::Local) rank_barrier<X>(p, s, p.exit_target);
+}
+
+}  // namespace tw

@@ -1,0 +1,260 @@
+"""K1 -- fused AllReduce + residual-add + RMSNorm on the GPU vs the oracle
+(weavesim::fused_allreduce_rmsnorm, proj/src/collectives.cpp:157-182).
+
+Ranks are simulated on one device (PEER transport over one communicator, the
+reference's in-process RankGroup, proj/include/weavesim/collectives.hpp:34-46);
+the NVLS transport needs >= 2 NVSwitch-attached GPUs and is exercised by the
+multi-GPU tests at the bottom when they are visible.
+
+Tolerances: fp32 -- residual shards bitwise (rank-ascending fp32 sum, same as
+proj/src/collectives.cpp:140-144), output <= 1e-5; bf16 -- residual shards
+bitwise equal to RNE(oracle r'), output 2e-2 relative (row-rms guarded)."""
+import numpy as np
+import pytest
+
+from tests.helpers import assert_abs_close, assert_bf16_close, bf16_round, group_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def setup_group(comm, inputs, residual, weight, ranges, dtype):
+    import torch
+    W, T, H = inputs.shape
+    for r in range(W):
+        comm.buffer(r, 0, (T, H), dtype).copy_(torch.from_numpy(inputs[r]).to(dtype))
+        comm.buffer(r, 1, (T, H), dtype).fill_(float("nan"))
+    shards = [torch.from_numpy(np.ascontiguousarray(residual[b:e])).to("cuda", dtype) for b, e in ranges]
+    weights = [torch.from_numpy(weight).cuda() for _ in range(W)]
+    return shards, weights
+
+
+def run_k1(inputs, residual, weight, dtype, ranges=None, gather=False, sm_budget=4, comm=None):
+    import torch
+    import paper_2505_11329_b200 as tw
+    W, T, H = inputs.shape
+    if ranges is None:
+        ranges = tw.token_shard_map(T, W)
+    own = comm is None
+    if own:
+        comm = tw.Communicator(W, [0] * W, max(T * H * 4, 1), tw.TW_TRANSPORT_PEER)
+    shards, weights = setup_group(comm, inputs, residual, weight, ranges, dtype)
+    comm.fused_allreduce_rmsnorm(T, H, shards, weights, shard_ranges=ranges, sm_budget=sm_budget,
+                                 gather_residual=gather, dtype=dtype)
+    torch.cuda.synchronize()
+    comm.check()
+    outs = [comm.buffer(r, 1, (T, H), dtype).float().cpu().numpy() for r in range(W)]
+    res = [s.float().cpu().numpy() for s in shards]
+    gathered = [comm.buffer(r, 2, (T, H), dtype).float().cpu().numpy() for r in range(W)] if gather else None
+    if own:
+        comm.close()
+    return outs, res, gathered
+
+
+def oracle_case(orc, inputs, residual, weight, ranges, bf16):
+    if bf16:
+        inputs, residual = bf16_round(inputs), bf16_round(residual)
+    shards = [residual[b:e] for b, e in ranges]
+    out, new = orc.fused_allreduce_rmsnorm(list(inputs), shards, weight, ranges)
+    return inputs, residual, out, new
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("T", [1, 3, 17, 40, 256])
+@pytest.mark.parametrize("H", [16, 24, 33, 64, 1024])
+def test_k1_fp32_matches_oracle(cuda, orc, world, T, H):
+    import torch
+    import paper_2505_11329_b200 as tw
+    inputs, residual, weight = group_inputs(77 * world + T + H, world, T, H)
+    ranges = tw.token_shard_map(T, world)
+    _, _, want_out, want_res = oracle_case(orc, inputs, residual, weight, ranges, False)
+    outs, res, _ = run_k1(inputs, residual, weight, torch.float32)
+    for r in range(world):
+        assert_abs_close(outs[r], want_out, 1e-5, f"rank {r} output")
+        assert np.array_equal(res[r], want_res[r]), f"rank {r} residual shard must be bitwise"
+        assert np.array_equal(outs[r], outs[0]), "replicated output must be identical on every rank"
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("T,H", [(1, 16), (17, 64), (40, 33), (256, 1024), (128, 8192), (64, 6144)])
+def test_k1_bf16_matches_oracle(cuda, orc, world, T, H):
+    import torch
+    import paper_2505_11329_b200 as tw
+    inputs, residual, weight = group_inputs(5 * world + T * 3 + H, world, T, H)
+    ranges = tw.token_shard_map(T, world)
+    inputs, residual, want_out, want_res = oracle_case(orc, inputs, residual, weight, ranges, True)
+    outs, res, _ = run_k1(inputs, residual, weight, torch.bfloat16)
+    for r in range(world):
+        assert_bf16_close(outs[r], want_out, what=f"rank {r} output")
+        assert np.array_equal(res[r], bf16_round(want_res[r])), f"rank {r} residual shard"
+
+
+def test_k1_matches_golden_fixtures(cuda, golden):
+    """The reference's own outputs (tests/golden, from oracle/_ref)."""
+    import torch
+    meta, arrays = golden
+    for case in meta["fused"]:
+        inputs, residual, weight = group_inputs(case["seed"], case["world"], case["T"], case["H"])
+        ranges = [tuple(r) for r in case["ranges"]]
+        outs, res, _ = run_k1(inputs, residual, weight, torch.float32, ranges=ranges)
+        assert_abs_close(outs[0], arrays[f"fused_{case['id']}_out"], 1e-5)
+        assert np.array_equal(np.concatenate(res), arrays[f"fused_{case['id']}_res"])
+
+
+@pytest.mark.parametrize("dtype_name", ["float32", "bfloat16"])
+def test_k1_gather_residual(cuda, orc, dtype_name):
+    """G=2 (north_star): r' is all-gathered to every rank's RESIDUAL buffer."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    dtype = getattr(torch, dtype_name)
+    W, T, H = 4, 37, 256
+    inputs, residual, weight = group_inputs(9, W, T, H)
+    ranges = tw.token_shard_map(T, W)
+    inputs, residual, want_out, want_res = oracle_case(orc, inputs, residual, weight, ranges,
+                                                       dtype == torch.bfloat16)
+    outs, res, gathered = run_k1(inputs, residual, weight, dtype, gather=True)
+    full = np.concatenate(want_res)
+    if dtype == torch.bfloat16:
+        full = bf16_round(full)
+    for r in range(W):
+        assert np.array_equal(gathered[r], full)
+
+
+def test_k1_uneven_and_empty_shards(cuda, orc):
+    """Custom shard maps, including empty ranges (T < N)."""
+    import torch
+    for W, T, ranges in [(8, 3, None), (4, 10, [(0, 7), (7, 7), (7, 9), (9, 10)]),
+                         (2, 9, [(0, 0), (0, 9)])]:
+        inputs, residual, weight = group_inputs(T + W, W, T, 64)
+        if ranges is None:
+            ranges = orc.token_shard_map(T, W)
+        _, _, want_out, want_res = oracle_case(orc, inputs, residual, weight, ranges, False)
+        outs, res, _ = run_k1(inputs, residual, weight, torch.float32, ranges=ranges)
+        for r in range(W):
+            assert_abs_close(outs[r], want_out, 1e-5)
+            assert np.array_equal(res[r].reshape(-1), want_res[r].reshape(-1))
+
+
+def test_k1_contract_and_shape_errors(cuda):
+    import torch
+    import paper_2505_11329_b200 as tw
+    W, T, H = 4, 8, 64
+    comm = tw.Communicator(W, [0] * W, T * H * 4, tw.TW_TRANSPORT_PEER)
+    shards = [torch.zeros(2, H, device="cuda") for _ in range(W)]
+    weights = [torch.ones(H, device="cuda") for _ in range(W)]
+    bad = [(0, 2), (1, 4), (4, 6), (6, 8)]  # overlap: proj/tests/test_collectives.cpp:154-156
+    with pytest.raises(tw.ContractError):
+        comm.fused_allreduce_rmsnorm(T, H, shards, weights, shard_ranges=bad)
+    with pytest.raises(tw.ContractError):
+        comm.fused_allreduce_rmsnorm(T, H, shards, weights, shard_ranges=[(0, 2), (2, 4), (4, 6), (6, 9)])
+    with pytest.raises(tw.DimensionError):  # exceeds the symmetric buffers
+        comm.fused_allreduce_rmsnorm(T * 2, H, shards, weights)
+    with pytest.raises(tw.NumericError):
+        comm.fused_allreduce_rmsnorm(T, H, shards, weights, eps=-1.0)
+    with pytest.raises(tw.ConfigError):
+        tw.Communicator(1, [0], 1024, tw.TW_TRANSPORT_PEER).fused_allreduce_rmsnorm(T, H, shards[:1], weights[:1])
+    comm.close()
+
+
+def test_k1_repeated_launches_and_budgets(cuda, orc):
+    """Signal-pad epochs stay consistent across many launches with varying
+    SM budgets and shapes on one communicator (no reset, no timeout)."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    W, H = 8, 512
+    comm = tw.Communicator(W, [0] * W, 300 * H * 4, tw.TW_TRANSPORT_PEER)
+    for it, (T, budget) in enumerate([(1, 1), (256, 2), (17, 4), (300, 8), (64, 16), (5, 3), (200, 12)] * 3):
+        inputs, residual, weight = group_inputs(it, W, T, H)
+        ranges = tw.token_shard_map(T, W)
+        inputs, residual, want_out, want_res = oracle_case(orc, inputs, residual, weight, ranges, True)
+        outs, res, _ = run_k1(inputs, residual, weight, torch.bfloat16, sm_budget=budget, comm=comm)
+        assert_bf16_close(outs[W - 1], want_out)
+    comm.check()
+    comm.close()
+
+
+def test_k3_allreduce_baseline(cuda, orc):
+    import torch
+    import paper_2505_11329_b200 as tw
+    W, T, H = 8, 100, 1024
+    inputs, _, _ = group_inputs(3, W, T, H)
+    comm = tw.Communicator(W, [0] * W, T * H * 4, tw.TW_TRANSPORT_PEER)
+    for r in range(W):
+        comm.buffer(r, 0, (T, H), torch.float32).copy_(torch.from_numpy(inputs[r]))
+    comm.allreduce(T, H, torch.float32, sm_budget=4)
+    torch.cuda.synchronize()
+    want = orc.all_reduce(list(inputs))
+    for r in range(W):
+        assert np.array_equal(comm.buffer(r, 1, (T, H), torch.float32).cpu().numpy(), want)
+    comm.close()
+
+
+def test_k1_full_size_llama_boundary_property(cuda, orc):
+    """C2 shape (N=8, T=1024, H=8192, bf16) on simulated ranks: the output is
+    the RMSNorm of the gathered residual (size-independent property) and a row
+    sample matches the oracle."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    W, T, H = 8, 1024, 8192
+    comm = tw.Communicator(W, [0] * W, T * H * 2, tw.TW_TRANSPORT_PEER)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    parts = [(torch.rand(T, H, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16) for _ in range(W)]
+    res_full = (torch.rand(T, H, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w = torch.rand(H, device="cuda", generator=g) + 0.5
+    ranges = tw.token_shard_map(T, W)
+    for r in range(W):
+        comm.buffer(r, 0, (T, H), torch.bfloat16).copy_(parts[r])
+    shards = [res_full[b:e].clone() for b, e in ranges]
+    comm.fused_allreduce_rmsnorm(T, H, shards, [w] * W, sm_budget=8, gather_residual=True)
+    torch.cuda.synchronize()
+    comm.check()
+    summed = sum(p.float() for p in parts)
+    want_res = (summed + res_full.float()).to(torch.bfloat16)
+    assert torch.equal(torch.cat(shards), want_res)
+    rb = want_res.float()
+    want = rb * torch.rsqrt((rb * rb).mean(1, keepdim=True) + 1e-5) * w
+    for r in range(W):
+        out = comm.buffer(r, 1, (T, H), torch.bfloat16).float()
+        rel = ((out - want).abs() / torch.maximum(want.abs(), want.pow(2).mean(1, keepdim=True).sqrt())).max()
+        assert rel.item() <= 2e-2
+        assert torch.equal(comm.buffer(r, 2, (T, H), torch.bfloat16), want_res)
+    # rows are independent: the oracle on a row sample (as its own T' problem)
+    rows = list(range(0, T, 131))
+    ins = np.stack([p[rows].float().cpu().numpy() for p in parts])
+    res_rows = res_full[rows].float().cpu().numpy()
+    sub = orc.token_shard_map(len(rows), W)
+    o, new = orc.fused_allreduce_rmsnorm(list(ins), [res_rows[b:e] for b, e in sub], w.cpu().numpy(), sub)
+    assert np.array_equal(bf16_round(np.concatenate(new)), want_res[rows].float().cpu().numpy())
+    assert_bf16_close(comm.buffer(0, 1, (T, H), torch.bfloat16)[rows].float().cpu().numpy(), o)
+    comm.close()
+
+
+@pytest.mark.skipif("__import__('torch').cuda.device_count() < 2")
+@pytest.mark.parametrize("dtype_name", ["float32", "bfloat16"])
+def test_k1_nvls_multi_gpu(cuda, orc, dtype_name):
+    import torch
+    import paper_2505_11329_b200 as tw
+    n = min(torch.cuda.device_count(), 8)
+    dtype = getattr(torch, dtype_name)
+    T, H = 257, 8192 if dtype == torch.bfloat16 else 1024
+    comm = tw.Communicator(n, list(range(n)), T * H * 4, tw.TW_TRANSPORT_NVLS)
+    inputs, residual, weight = group_inputs(21, n, T, H)
+    ranges = tw.token_shard_map(T, n)
+    inputs, residual, want_out, want_res = oracle_case(orc, inputs, residual, weight, ranges, dtype == torch.bfloat16)
+    shards, weights = [], []
+    for r in range(n):
+        comm.buffer(r, 0, (T, H), dtype).copy_(torch.from_numpy(inputs[r]).to(dtype))
+        b, e = ranges[r]
+        shards.append(torch.from_numpy(np.ascontiguousarray(residual[b:e])).to(f"cuda:{r}", dtype))
+        weights.append(torch.from_numpy(weight).to(f"cuda:{r}"))
+    comm.fused_allreduce_rmsnorm(T, H, shards, weights, sm_budget=8, gather_residual=True,
+                                 streams=[torch.cuda.current_stream(r) for r in range(n)])
+    for r in range(n):
+        torch.cuda.synchronize(r)
+    comm.check()
+    for r in range(n):
+        out = comm.buffer(r, 1, (T, H), dtype).float().cpu().numpy()
+        if dtype == torch.float32:
+            assert_abs_close(out, want_out, 1e-5)
+        else:
+            assert_bf16_close(out, want_out)
+    comm.close()

@@ -1,0 +1,147 @@
+"""K2 -- TP=1 fused residual-add + RMSNorm on the GPU vs the oracle
+(weavesim::rmsnorm_residual, proj/src/numerics.cpp:30-64).
+
+Tolerances (north_star): fp32 storage -- residual_out bitwise (same fp32 add),
+output <= 1e-5 absolute; bf16 storage -- residual_out bitwise equal to the
+RNE-rounded oracle r', output within 2e-2 relative (row-rms guarded)."""
+import numpy as np
+import pytest
+
+from tests.helpers import assert_abs_close, assert_bf16_close, bf16_round, norm_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def run_k2(inp, res, w, dtype, eps=1e-5, sm_budget=0, inplace=False):
+    import torch
+    import paper_2505_11329_b200 as tw
+    ti = torch.from_numpy(inp).to("cuda", dtype)
+    tr = torch.from_numpy(res).to("cuda", dtype)
+    tw_ = torch.from_numpy(w).to("cuda", torch.float32)
+    out, rout = tw.rmsnorm_residual(ti, tr, tw_, eps, residual_out=tr if inplace else None, sm_budget=sm_budget)
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy(), rout.float().cpu().numpy()
+
+
+@pytest.mark.parametrize("T,H", [(1, 8), (5, 16), (17, 33), (64, 128), (3, 1024), (33, 4096), (64, 8192),
+                                 (7, 12), (9, 24), (2, 16384)])
+def test_k2_fp32_matches_oracle(cuda, orc, T, H):
+    inp, res, w = norm_inputs(11 + T * 7 + H, T, H)
+    want_out, want_res = orc.rmsnorm_residual(inp, res, w)
+    import torch
+    out, rout = run_k2(inp, res, w, torch.float32)
+    assert np.array_equal(rout, want_res), "r' must be the same fp32 add"
+    assert_abs_close(out, want_out, 1e-5)
+
+
+@pytest.mark.parametrize("T,H", [(1, 8), (5, 16), (17, 33), (64, 128), (64, 8192), (7, 24), (256, 8192),
+                                 (4, 6144), (3, 16384)])
+def test_k2_bf16_matches_oracle(cuda, orc, T, H):
+    import torch
+    inp, res, w = norm_inputs(5 + T + H, T, H)
+    inp, res = bf16_round(inp), bf16_round(res)
+    want_out, want_res = orc.rmsnorm_residual(inp, res, w)
+    out, rout = run_k2(inp, res, w, torch.bfloat16)
+    assert np.array_equal(rout, bf16_round(want_res)), "bf16 r' must be RNE(fp32 r')"
+    assert_bf16_close(out, want_out)
+
+
+def test_k2_in_place_residual(cuda, orc):
+    import torch
+    inp, res, w = norm_inputs(3, 40, 8192)
+    inp, res = bf16_round(inp), bf16_round(res)
+    want_out, want_res = orc.rmsnorm_residual(inp, res, w)
+    out, rout = run_k2(inp, res, w, torch.bfloat16, inplace=True)
+    assert np.array_equal(rout, bf16_round(want_res))
+    assert_bf16_close(out, want_out)
+
+
+def test_k2_unaligned_pointers_take_the_scalar_path(cuda, orc):
+    import torch
+    import paper_2505_11329_b200 as tw
+    T, H = 6, 64
+    inp, res, w = norm_inputs(17, T, H)
+    want_out, want_res = orc.rmsnorm_residual(inp, res, w)
+    big_i = torch.zeros(T * H + 1, device="cuda")
+    big_r = torch.zeros(T * H + 1, device="cuda")
+    ti = big_i[1:].view(T, H)
+    tr = big_r[1:].view(T, H)
+    ti.copy_(torch.from_numpy(inp))
+    tr.copy_(torch.from_numpy(res))
+    out, rout = tw.rmsnorm_residual(ti, tr, torch.from_numpy(w).cuda())
+    assert np.array_equal(rout.cpu().numpy(), want_res)
+    assert_abs_close(out.cpu().numpy(), want_out, 1e-5)
+
+
+def test_k2_zero_input_normalizes_to_zero(cuda):
+    import torch
+    import paper_2505_11329_b200 as tw
+    z = torch.zeros(3, 8, device="cuda")
+    out, rout = tw.rmsnorm_residual(z, z, torch.ones(8, device="cuda"))
+    assert torch.all(out == 0) and torch.all(rout == 0)
+
+
+def test_k2_row_locality(cuda):
+    """proj/tests/test_numerics.cpp:100-115: scaling one row leaves the others unchanged."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    x = torch.randn(4, 16, device="cuda")
+    r = torch.zeros(4, 16, device="cuda")
+    w = torch.ones(16, device="cuda")
+    base, _ = tw.rmsnorm_residual(x, r, w)
+    x2 = x.clone()
+    x2[2] *= 8
+    changed, _ = tw.rmsnorm_residual(x2, r, w)
+    keep = [0, 1, 3]
+    assert torch.equal(base[keep], changed[keep])
+
+
+def test_k2_errors(cuda):
+    import torch
+    import paper_2505_11329_b200 as tw
+    a = torch.zeros(2, 8, device="cuda")
+    b = torch.zeros(3, 8, device="cuda")
+    with pytest.raises(tw.DimensionError):
+        tw.rmsnorm_residual(a, b, torch.ones(8, device="cuda"))
+    with pytest.raises(tw.DimensionError):
+        tw.rmsnorm_residual(a, a, torch.ones(7, device="cuda"))
+    with pytest.raises(tw.NumericError):
+        tw.rmsnorm_residual(a, a, torch.ones(8, device="cuda"), eps=-1.0)
+    out, rout = tw.rmsnorm_residual(a[:0], a[:0], torch.ones(8, device="cuda"))
+    assert out.shape == (0, 8)
+
+
+def test_k2_sm_budget_does_not_change_results(cuda):
+    import torch
+    import paper_2505_11329_b200 as tw
+    x = torch.randn(300, 8192, device="cuda", dtype=torch.bfloat16)
+    r = torch.randn(300, 8192, device="cuda", dtype=torch.bfloat16)
+    w = torch.rand(8192, device="cuda") + 0.5
+    ref_out, ref_res = tw.rmsnorm_residual(x, r, w)
+    for budget in (1, 2, 8, 16, 148):
+        o, rr = tw.rmsnorm_residual(x, r, w, sm_budget=budget)
+        assert torch.equal(o, ref_out) and torch.equal(rr, ref_res)
+
+
+def test_k2_full_size_vs_torch_fp32_and_sampled_oracle(cuda, orc):
+    """Bench shape (8192 x 8192 bf16): torch fp32 restatement over every row,
+    and the C oracle on a sample of rows."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    T, H = 8192, 8192
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = (torch.rand(T, H, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    r = (torch.rand(T, H, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w = torch.rand(H, device="cuda", generator=g) + 0.5
+    out, rout = tw.rmsnorm_residual(x, r, w)
+    rp = x.float() + r.float()
+    assert torch.equal(rout, rp.to(torch.bfloat16))
+    rb = rout.float()
+    want = rb * torch.rsqrt((rb * rb).mean(dim=1, keepdim=True) + 1e-5) * w
+    assert_bf16_close(out[::97].float().cpu().numpy(), want[::97].cpu().numpy())
+    err = ((out.float() - want).abs() / torch.maximum(want.abs(), want.pow(2).mean(1, keepdim=True).sqrt())).max()
+    assert err.item() <= 2e-2
+    rows = torch.arange(0, T, 509, device="cuda")
+    o2, r2 = orc.rmsnorm_residual(x[rows].float().cpu().numpy(), r[rows].float().cpu().numpy(), w.cpu().numpy())
+    assert np.array_equal(rout[rows].float().cpu().numpy(), bf16_round(r2))
+    assert_bf16_close(out[rows].float().cpu().numpy(), o2)
