@@ -1,0 +1,195 @@
+// tw_bulk.cuh -- K2 (TP=1 fused residual-add + RMSNorm) as a warp-specialised
+// bulk-copy pipeline for sm_100a.
+//
+// Persistent grid, one CTA per SM.  Warp 0 lane 0 is the producer: for each
+// row it owns it arms a full-barrier with the row's byte count and issues two
+// cp.async.bulk (TMA bulk engine) copies, input row and residual row, into a
+// ring of S shared-memory stages (S*2*row_bytes <= ~200 KB).  The remaining
+// warps are consumers: wait on the stage's full barrier, read the row from
+// shared memory, r' = x + res (stored to global as soon as it is formed), hand
+// the stage back (empty barrier), reduce the sum of squares across the
+// consumer warps (one named barrier), and store out = r' * inv_rms * w with w
+// held in registers for the whole kernel.  HBM traffic is exactly the
+// algorithmic 4*T*H*elem bytes; up to S rows per SM are in flight.
+#pragma once
+
+#include <cstdint>
+
+#include "tw_ptx.cuh"
+#include "tw_rownorm.cuh"
+
+namespace tw {
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+// Global -> shared bulk copy completing on an mbarrier (TMA bulk engine).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ uint4 lds_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_addr(p)));
+  return v;
+}
+
+struct BulkParams {
+  const void* in;
+  const void* res_in;
+  void* res_out;
+  void* out;
+  const float* weight;
+  long long T, H;
+  int V;       // 16-byte vectors per row
+  int tpr;     // consumer threads (multiple of 32)
+  int stages;  // smem ring depth
+  uint32_t row_bytes;
+  float eps;
+};
+
+constexpr int kBulkMaxConsumers = 512;
+
+template <class E, int VPT>
+__global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_bulk_kernel(const __grid_constant__ BulkParams p) {
+  constexpr int N = 16 / sizeof(E);
+  using VT = Vec<E, N>;
+  using Acc = typename std::conditional<sizeof(E) == 4, double, float>::type;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int S = p.stages;
+  unsigned char* ring = smem;  // [S][2][row_bytes]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(S) * 2 * p.row_bytes);
+  uint64_t* empty = full + S;
+  Acc* part = reinterpret_cast<Acc*>(empty + S);  // [2][consumer warps]
+
+  const int tpr = p.tpr;
+  const int cwarps = tpr >> 5;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], cwarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const long long nrows = p.T > blockIdx.x ? (p.T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp == 0) {
+    // ---- producer ----
+    if (lane == 0) {
+      for (long long i = 0; i < nrows; ++i) {
+        const int s = static_cast<int>(i % S);
+        const uint32_t ph = static_cast<uint32_t>((i / S) & 1);
+        if (i >= S) mbar_wait(&empty[s], ph ^ 1u);
+        const long long row = blockIdx.x + i * gridDim.x;
+        unsigned char* dst = ring + static_cast<size_t>(s) * 2 * p.row_bytes;
+        mbar_arrive_expect_tx(&full[s], 2 * p.row_bytes);
+        bulk_g2s(dst, static_cast<const unsigned char*>(p.in) + row * p.row_bytes, p.row_bytes, &full[s]);
+        bulk_g2s(dst + p.row_bytes, static_cast<const unsigned char*>(p.res_in) + row * p.row_bytes, p.row_bytes,
+                 &full[s]);
+      }
+    }
+    return;
+  }
+
+  // ---- consumers ----
+  const int lt = threadIdx.x - 32;
+  const int cw = warp - 1;
+  float w[VPT][N];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int c = lt + k * tpr;
+    if (c < p.V) load_weight<N>(p.weight, static_cast<long long>(c) * N, w[k]);
+  }
+  for (long long i = 0; i < nrows; ++i) {
+    const int s = static_cast<int>(i % S);
+    const uint32_t ph = static_cast<uint32_t>((i / S) & 1);
+    const long long row = blockIdx.x + i * gridDim.x;
+    const long long rowe = row * p.H;
+    const unsigned char* src = ring + static_cast<size_t>(s) * 2 * p.row_bytes;
+    mbar_wait(&full[s], ph);
+    typename VT::Raw rr[VPT];
+    Acc ss = 0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int c = lt + k * tpr;
+      if (c < p.V) {
+        float x[N], r[N];
+        VT::unpack(lds_v4(src + c * 16), x);
+        VT::unpack(lds_v4(src + p.row_bytes + c * 16), r);
+#pragma unroll
+        for (int j = 0; j < N; ++j) r[j] = x[j] + r[j];
+        rr[k] = VT::pack(r);
+        VT::unpack(rr[k], r);
+#pragma unroll
+        for (int j = 0; j < N; ++j) ss += static_cast<Acc>(r[j]) * static_cast<Acc>(r[j]);
+        VT::store(p.res_out, rowe + static_cast<long long>(c) * N, rr[k]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);  // stage free for the producer
+    ss = warp_sum(ss);
+    Acc total;
+    if (cwarps == 1) {
+      total = ss;
+    } else {
+      Acc* pp = part + (i & 1) * cwarps;
+      if (lane == 0) pp[cw] = ss;
+      named_bar_sync(1, tpr);
+      total = 0;
+      for (int q = 0; q < cwarps; ++q) total += pp[q];
+    }
+    const float inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(p.H)) + p.eps);
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int c = lt + k * tpr;
+      if (c < p.V) {
+        float o[N];
+        VT::unpack(rr[k], o);
+#pragma unroll
+        for (int j = 0; j < N; ++j) o[j] = o[j] * inv * w[k][j];
+        VT::store(p.out, rowe + static_cast<long long>(c) * N, VT::pack(o));
+      }
+    }
+  }
+}
+
+}  // namespace tw

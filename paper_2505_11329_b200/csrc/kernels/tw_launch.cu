@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cstdint>
 
+#include "tw_bulk.cuh"
 #include "tw_launch.h"
 #include "tw_rownorm.cuh"
 
@@ -136,6 +137,39 @@ int rownorm_blocks_per_sm(const RowPlan& plan, bool bf16, Xport x) {
                                                     0) != cudaSuccess)
     return 0;
   return n;
+}
+
+// ---- K2 bulk-copy pipeline -------------------------------------------------------
+
+namespace {
+using BulkFn = void (*)(BulkParams);
+
+template <class E>
+BulkFn pick_bulk_e(int vpt) {
+  switch (vpt) {
+    case 1: return k2_bulk_kernel<E, 1>;
+    case 2: return k2_bulk_kernel<E, 2>;
+    case 4: return k2_bulk_kernel<E, 4>;
+    case 8: return k2_bulk_kernel<E, 8>;
+    default: return nullptr;
+  }
+}
+}  // namespace
+
+size_t bulk_smem_bytes(int stages, uint32_t row_bytes, int tpr) {
+  return static_cast<size_t>(stages) * 2 * row_bytes + 2 * stages * sizeof(uint64_t) + 2 * (tpr / 32) * sizeof(double);
+}
+
+cudaError_t launch_k2_bulk(const BulkParams& params, int vpt, bool bf16, int grid, cudaStream_t stream) {
+  BulkFn fn = bf16 ? pick_bulk_e<uint16_t>(vpt) : pick_bulk_e<float>(vpt);
+  if (!fn) return cudaErrorInvalidConfiguration;
+  const size_t smem = bulk_smem_bytes(params.stages, params.row_bytes, params.tpr);
+  cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  BulkParams p = params;
+  void* args[] = {&p};
+  return cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(params.tpr + 32), args, smem, stream);
 }
 
 // ---- finite scan (TokenMatrix::validate, numerics.cpp:25-27) ---------------------
