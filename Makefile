@@ -19,9 +19,9 @@ HHDR := $(PKG)/csrc/host/tw_internal.h include/tw/tw.h
 SHIM_SRC := $(wildcard $(PKG)/csrc/host/weavesim_*.cpp)
 SHIM_HDR := $(wildcard include/weavesim/*.hpp)
 
-.PHONY: all lib shim oracle ref clean
+.PHONY: all lib shim oracle ref cpptests clean
 
-all: lib shim oracle
+all: lib shim oracle cpptests
 
 lib: $(LIBDIR)/libtw.so
 
@@ -42,6 +42,13 @@ shim: $(LIBDIR)/libweavesim_b200.so
 
 $(LIBDIR)/libweavesim_b200.so: $(SHIM_SRC) $(SHIM_HDR) $(LIBDIR)/libtw.so
 	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -o $@ $(SHIM_SRC) -L$(LIBDIR) -ltw -Wl,-rpath,'$$ORIGIN' -pthread
+
+# The reference's own test cases compiled against the drop-in library.
+cpptests: build/tests/test_dropin
+
+build/tests/test_dropin: tests/cpp/test_dropin.cpp $(SHIM_HDR) $(LIBDIR)/libweavesim_b200.so
+	@mkdir -p build/tests
+	$(CXX) -std=c++20 -O2 -Iinclude -o $@ $< -L$(LIBDIR) -lweavesim_b200 -ltw -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)'
 
 oracle:
 	$(MAKE) -C oracle oracle

@@ -140,6 +140,13 @@ TW_API tw_status tw_fused_allreduce_rmsnorm_group(tw_comm_t comm, int64_t T, int
 TW_API tw_status tw_allreduce_group(tw_comm_t comm, int64_t T, int64_t H, tw_dtype dtype, int sm_budget,
                              void* const* streams);
 
+/* --- Device memory helpers (so C/C++ hosts need no CUDA headers) ------------
+ * tw_memcpy uses unified addressing (direction inferred); stream NULL = sync. */
+TW_API tw_status tw_device_alloc(int device, size_t bytes, void** ptr);
+TW_API tw_status tw_device_free(int device, void* ptr);
+TW_API tw_status tw_memcpy(void* dst, const void* src, size_t bytes, void* stream);
+TW_API tw_status tw_device_synchronize(int device);
+
 /* Per-rank async error flag set by the in-kernel bounded barrier spin.
  * Returns TW_ERR_TIMEOUT (and clears the flag) if any rank timed out. */
 TW_API tw_status tw_comm_check(tw_comm_t comm);

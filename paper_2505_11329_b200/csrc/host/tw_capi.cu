@@ -18,11 +18,17 @@
 namespace tw {
 
 namespace {
-thread_local std::string g_last_error;
+// POD storage: safe to touch from static destructors of other libraries
+// (a thread_local std::string may already be destroyed at process exit).
+thread_local char g_last_error[1024];
 }
 
-void set_error(const std::string& msg) { g_last_error = msg; }
-void clear_error() { g_last_error.clear(); }
+void set_error(const std::string& msg) {
+  const size_t n = std::min(msg.size(), sizeof(g_last_error) - 1);
+  std::memcpy(g_last_error, msg.data(), n);
+  g_last_error[n] = '\0';
+}
+void clear_error() { g_last_error[0] = '\0'; }
 
 tw_status fail(tw_status code, const std::string& msg) {
   set_error(msg);
@@ -249,7 +255,7 @@ extern "C" {
 
 int tw_abi_version(void) { return TW_ABI_VERSION; }
 const char* tw_version(void) { return "tokenweave-b200 0.1 (sm_100a)"; }
-const char* tw_last_error(void) { return g_last_error.c_str(); }
+const char* tw_last_error(void) { return g_last_error; }
 
 int tw_device_count(void) {
   int n = 0;
@@ -434,6 +440,48 @@ tw_status tw_comm_multicast_buffer(tw_comm_t comm, int rank, tw_buffer which, vo
   if (rank < 0 || rank >= comm->world) return fail(TW_ERR_CONFIG, "comm_multicast_buffer: rank out of range");
   if (which < TW_BUF_INPUT || which > TW_BUF_RESIDUAL) return fail(TW_ERR_CONFIG, "bad buffer id");
   *device_ptr = comm->ranks[rank].mc_buf[which];
+  return TW_OK;
+}
+
+tw_status tw_device_alloc(int device, size_t bytes, void** ptr) {
+  clear_error();
+  if (!ptr) return fail(TW_ERR_CONFIG, "device_alloc: null output");
+  *ptr = nullptr;
+  DeviceGuard guard;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "device_alloc: cudaSetDevice");
+  if (bytes == 0) return TW_OK;
+  e = cudaMalloc(ptr, bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "device_alloc: cudaMalloc");
+  return TW_OK;
+}
+
+tw_status tw_device_free(int device, void* ptr) {
+  clear_error();
+  if (!ptr) return TW_OK;
+  DeviceGuard guard;
+  cudaSetDevice(device);
+  cudaError_t e = cudaFree(ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "device_free");
+  return TW_OK;
+}
+
+tw_status tw_memcpy(void* dst, const void* src, size_t bytes, void* stream) {
+  clear_error();
+  if (bytes == 0) return TW_OK;
+  if (!dst || !src) return fail(TW_ERR_CONFIG, "memcpy: null pointer");
+  cudaError_t e = stream ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream))
+                         : cudaMemcpy(dst, src, bytes, cudaMemcpyDefault);
+  if (e != cudaSuccess) return cuda_fail(e, "memcpy");
+  return TW_OK;
+}
+
+tw_status tw_device_synchronize(int device) {
+  clear_error();
+  DeviceGuard guard;
+  cudaSetDevice(device);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "device_synchronize");
   return TW_OK;
 }
 

@@ -1,0 +1,264 @@
+// test_dropin.cpp -- the reference's own test cases for the hot-path API,
+// restated against the drop-in build (libweavesim_b200.so): the same source a
+// reference user compiles, linked against the B200 library instead.
+//
+//   test_dropin host   -> validation / exception / planner cases (no GPU)
+//   test_dropin gpu    -> + numerical cases that run the sm_100a kernels
+//
+// Cases follow proj/tests/test_numerics.cpp, test_collectives.cpp,
+// test_splitter.cpp and acceptance.cpp check 1 (cited per case).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <random>
+#include <string>
+
+#include "weavesim/collectives.hpp"
+#include "weavesim/errors.hpp"
+#include "weavesim/numerics.hpp"
+#include "weavesim/splitter.hpp"
+
+using namespace weavesim;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                          \
+  do {                                                                       \
+    if (cond) {                                                              \
+      ++g_pass;                                                              \
+    } else {                                                                 \
+      ++g_fail;                                                              \
+      std::printf("FAIL %s:%d  %s\n", __FILE__, __LINE__, #cond);            \
+    }                                                                        \
+  } while (0)
+#define CHECK_THROWS_AS(expr, Type)                                          \
+  do {                                                                       \
+    bool ok_ = false;                                                        \
+    try {                                                                    \
+      (void)(expr);                                                          \
+    } catch (const Type&) {                                                  \
+      ok_ = true;                                                            \
+    } catch (...) {                                                          \
+    }                                                                        \
+    CHECK(ok_ && #Type);                                                     \
+  } while (0)
+
+namespace {
+
+TokenMatrix random_matrix(std::int64_t t, std::int64_t h, std::mt19937_64& rng, float lo, float hi) {
+  std::uniform_real_distribution<float> d(lo, hi);
+  TokenMatrix m = TokenMatrix::zeros(t, h);
+  for (float& v : m.values) v = d(rng);
+  return m;
+}
+
+RankGroup random_group(int world, std::int64_t tokens, std::int64_t hidden, std::uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  RankGroup g;
+  g.world_size = world;
+  for (int r = 0; r < world; ++r) g.inputs.push_back(random_matrix(tokens, hidden, rng, -1.f, 1.f));
+  for (const TokenRange& range : token_shard_map(tokens, world).ranges)
+    g.residual_shards.push_back(random_matrix(range.size(), hidden, rng, -1.f, 1.f));
+  return g;
+}
+
+NormParams unit_norm(std::int64_t h) {
+  NormParams p;
+  p.weight.assign(static_cast<size_t>(h), 1.0f);
+  return p;
+}
+
+void host_cases() {
+  // test_numerics.cpp:39-60
+  TokenMatrix m = TokenMatrix::zeros(7, 5);
+  CHECK(m.values.size() == 35);
+  TokenMatrix bad = TokenMatrix::zeros(2, 3);
+  bad.values.pop_back();
+  CHECK_THROWS_AS(bad.validate(), DimensionError);
+  TokenMatrix nan = TokenMatrix::zeros(2, 3);
+  nan.values[1] = std::nanf("");
+  CHECK_THROWS_AS(nan.validate(), NumericError);
+  // test_numerics.cpp:117-126
+  NormParams p8 = unit_norm(8);
+  CHECK_THROWS_AS(rmsnorm_residual(TokenMatrix::zeros(2, 8), TokenMatrix::zeros(3, 8), p8), DimensionError);
+  NormParams p7 = unit_norm(7);
+  CHECK_THROWS_AS(rmsnorm_residual(TokenMatrix::zeros(2, 8), TokenMatrix::zeros(2, 8), p7), DimensionError);
+  // test_collectives.cpp:40-70
+  for (std::int64_t T : {0, 1, 7, 8, 100, 1023}) {
+    for (int W : {2, 3, 4, 8}) {
+      ShardMap map = token_shard_map(T, W);
+      CHECK(map.world_size() == W && map.total_tokens() == T);
+      bool ok = true;
+      for (const TokenRange& r : map.ranges) ok = ok && r.size() >= T / W && r.size() <= T / W + 1;
+      CHECK(ok);
+      map.validate(T);
+    }
+  }
+  CHECK_THROWS_AS(token_shard_map(16, 1), ConfigError);
+  CHECK_THROWS_AS(token_shard_map(-1, 4), DimensionError);
+  ShardMap sm = token_shard_map(16, 4);
+  CHECK_THROWS_AS(sm.validate(17), ContractError);
+  ShardMap ov = sm;
+  ov.ranges[2].begin -= 1;
+  CHECK_THROWS_AS(ov.validate(16), ContractError);
+  CHECK_THROWS_AS(ShardMap{}.validate(0), ContractError);
+  // test_collectives.cpp:129-161 (validation precedes any device work)
+  RankGroup g = random_group(4, 8, 8, 3);
+  const ShardMap shards = token_shard_map(8, 4);
+  RankGroup wrong_count = g;
+  wrong_count.inputs.pop_back();
+  CHECK_THROWS_AS(all_reduce(wrong_count), DimensionError);
+  RankGroup bad_res = g;
+  bad_res.residual_shards[1] = TokenMatrix::zeros(5, 8);
+  CHECK_THROWS_AS(fused_allreduce_rmsnorm(bad_res, unit_norm(8), shards), DimensionError);
+  ShardMap corrupt = shards;
+  corrupt.ranges[1].begin -= 1;
+  CHECK_THROWS_AS(fused_allreduce_rmsnorm(g, unit_norm(8), corrupt), ContractError);
+  CHECK_THROWS_AS(fused_allreduce_rmsnorm(g, unit_norm(7), shards), DimensionError);
+  const ShardMap s10 = token_shard_map(10, 2);
+  std::vector<TokenMatrix> wrong = {TokenMatrix::zeros(5, 4), TokenMatrix::zeros(4, 4)};
+  CHECK_THROWS_AS(all_gather(wrong, s10), DimensionError);
+  // test_splitter.cpp:21-32, 34-47, 128-150
+  SplitPolicy dense;
+  CHECK(select_mode(1023, dense) == SplitMode::FusedOnly);
+  CHECK(select_mode(1024, dense) == SplitMode::Overlap);
+  HardwareProfile p;
+  p.tile_tokens = 128;
+  p.cta_columns = 4;
+  const std::int64_t T = 9600, prefix = T / 2 + smart_offset_analytic(T, p);
+  CHECK(cta_count(prefix, p) == 132);
+  CHECK(wave_count(cta_count(prefix, p), p.num_sms) + wave_count(cta_count(T - prefix, p), p.num_sms) == 3);
+  SplitPlan plan;
+  plan.total_tokens = 100;
+  plan.prefix_tokens = 55;
+  plan = place_sequence_boundaries({30, 40, 30}, plan);
+  CHECK((plan.prefix_len_per_sequence == std::vector<std::int64_t>{30, 25, 0}));
+  CHECK_THROWS_AS(place_sequence_boundaries({30, 40}, plan), ContractError);
+  // SURVEY.md Appendix A (B200 geometry, dense threshold 1024)
+  const SplitPlan b = make_split_plan(4096, b200_geometry(), dense);
+  CHECK(b.prefix_tokens == 1152 && b.suffix_tokens == 2944 && b.offset == -896 && b.mode == SplitMode::Overlap);
+  CHECK(make_split_plan(512, b200_geometry(), dense).mode == SplitMode::FusedOnly);
+  // Alg. 1 sweep tie rules (test_splitter.cpp:83-101)
+  SplitPolicy grid;
+  CHECK(smart_offset_sweep(4096, grid, [](std::int64_t, std::int64_t) { return 1.0; }) == 0);
+  CHECK(smart_offset_sweep(4096, grid, [](std::int64_t a, std::int64_t) { return a == 2048 + 128 ? 0.5 : 1.0; }) ==
+        128);
+  CHECK(smart_offset_sweep(64, grid, [](std::int64_t, std::int64_t) { return 1.0; }) == 0);
+}
+
+void gpu_cases() {
+  // test_numerics.cpp:62-89 -- vs an independent double-precision restatement
+  std::mt19937_64 rng(7);
+  for (auto [T, H] : {std::pair<std::int64_t, std::int64_t>{1, 8}, {5, 16}, {17, 33}, {64, 128}}) {
+    const TokenMatrix in = random_matrix(T, H, rng, -2.f, 2.f);
+    const TokenMatrix res = random_matrix(T, H, rng, -2.f, 2.f);
+    NormParams params;
+    std::uniform_real_distribution<float> wd(0.5f, 1.5f);
+    params.weight.resize(static_cast<size_t>(H));
+    for (float& w : params.weight) w = wd(rng);
+    const NormResult r = rmsnorm_residual(in, res, params);
+    bool ok = true;
+    for (std::int64_t t = 0; t < T; ++t) {
+      double ss = 0;
+      for (std::int64_t j = 0; j < H; ++j) {
+        const double v = double(in.at(t, j)) + res.at(t, j);
+        ss += v * v;
+      }
+      const double inv = 1.0 / std::sqrt(ss / H + params.epsilon);
+      for (std::int64_t j = 0; j < H; ++j) {
+        const double want = (double(in.at(t, j)) + res.at(t, j)) * inv * params.weight[j];
+        ok = ok && std::abs(r.output.at(t, j) - want) <= 1e-5;
+        ok = ok && r.residual_out.at(t, j) == in.at(t, j) + res.at(t, j);
+      }
+    }
+    CHECK(ok);
+  }
+  // test_numerics.cpp:91-98
+  NormParams p8 = unit_norm(8);
+  const NormResult z = rmsnorm_residual(TokenMatrix::zeros(3, 8), TokenMatrix::zeros(3, 8), p8);
+  bool zero = true;
+  for (float v : z.output.values) zero = zero && v == 0.0f;
+  CHECK(zero);
+  // test_collectives.cpp:72-92
+  RankGroup g = random_group(4, 9, 12, 5);
+  const TokenMatrix sum = all_reduce(g);
+  bool exact = true;
+  for (std::int64_t i = 0; i < 9 * 12; ++i) {
+    float e = 0.0f;
+    for (const TokenMatrix& m : g.inputs) e += m.values[i];
+    exact = exact && sum.values[i] == e;
+  }
+  CHECK(exact);
+  for (std::int64_t tokens : {1, 7, 64, 129}) {
+    RankGroup gg = random_group(8, tokens, 16, 1000 + tokens);
+    const ShardMap shards = token_shard_map(tokens, 8);
+    CHECK(all_reduce(gg).values == all_gather(reduce_scatter(gg, shards), shards).values);
+  }
+  // test_collectives.cpp:94-114 -- fused vs unfused composition
+  for (int world : {2, 4, 8}) {
+    for (std::int64_t tokens : {1, 3, 17, 40}) {
+      RankGroup group = random_group(world, tokens, 32, 77 * world + tokens);
+      const ShardMap shards = token_shard_map(tokens, world);
+      const NormParams params = unit_norm(32);
+      const TokenMatrix reduced = all_reduce(group);
+      const TokenMatrix residual = all_gather(group.residual_shards, shards);
+      const NormResult oracle = rmsnorm_residual(reduced, residual, params);
+      const TokenMatrix fused = fused_allreduce_rmsnorm(group, params, shards);
+      bool ok = fused.values.size() == oracle.output.values.size();
+      for (size_t i = 0; ok && i < fused.values.size(); ++i)
+        ok = std::abs(fused.values[i] - oracle.output.values[i]) <= 1e-5;
+      CHECK(ok);
+      CHECK(all_gather(group.residual_shards, shards).values == oracle.residual_out.values);
+    }
+  }
+  // test_collectives.cpp:116-127 -- parallel flag is bitwise neutral
+  RankGroup seq = random_group(8, 53, 24, 99);
+  RankGroup par = seq;
+  const ShardMap s53 = token_shard_map(53, 8);
+  const TokenMatrix a = fused_allreduce_rmsnorm(seq, unit_norm(24), s53, false);
+  const TokenMatrix b = fused_allreduce_rmsnorm(par, unit_norm(24), s53, true);
+  CHECK(a.values == b.values);
+  for (int r = 0; r < 8; ++r) CHECK(seq.residual_shards[r].values == par.residual_shards[r].values);
+  // acceptance.cpp:37-86 (slice of the grid: 1e-5 vs the unfused chain)
+  double max_err = 0;
+  for (int world : {2, 4, 8})
+    for (std::int64_t tokens : {1, 3, 17, 256})
+      for (std::int64_t hidden : {16, 64, 1024})
+        for (int seed = 0; seed < 2; ++seed) {
+          std::mt19937_64 r2((std::uint64_t(world) << 48) ^ (std::uint64_t(tokens) << 24) ^
+                             (std::uint64_t(hidden) << 8) ^ std::uint64_t(seed));
+          std::uniform_real_distribution<float> d(-1.f, 1.f);
+          RankGroup grp;
+          grp.world_size = world;
+          for (int q = 0; q < world; ++q) {
+            TokenMatrix m = TokenMatrix::zeros(tokens, hidden);
+            for (float& v : m.values) v = d(r2);
+            grp.inputs.push_back(std::move(m));
+          }
+          const ShardMap sh = token_shard_map(tokens, world);
+          for (const TokenRange& rg : sh.ranges) {
+            TokenMatrix m = TokenMatrix::zeros(rg.size(), hidden);
+            for (float& v : m.values) v = d(r2);
+            grp.residual_shards.push_back(std::move(m));
+          }
+          NormParams prm;
+          prm.weight.resize(static_cast<size_t>(hidden));
+          std::uniform_real_distribution<float> wd(0.5f, 1.5f);
+          for (float& w : prm.weight) w = wd(r2);
+          const NormResult orc = rmsnorm_residual(all_reduce(grp), all_gather(grp.residual_shards, sh), prm);
+          const TokenMatrix fused = fused_allreduce_rmsnorm(grp, prm, sh);
+          for (size_t i = 0; i < fused.values.size(); ++i)
+            max_err = std::max(max_err, double(std::abs(fused.values[i] - orc.output.values[i])));
+        }
+  std::printf("acceptance-slice max_abs_err=%.3g\n", max_err);
+  CHECK(max_err <= 1e-5);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  const bool gpu = argc > 1 && std::strcmp(argv[1], "gpu") == 0;
+  host_cases();
+  if (gpu) gpu_cases();
+  std::printf("%s: %d passed, %d failed\n", gpu ? "gpu" : "host", g_pass, g_fail);
+  return g_fail ? 1 : 0;
+}

@@ -1,0 +1,34 @@
+"""The drop-in C++ API: the reference's own test cases (restated in
+tests/cpp/test_dropin.cpp) compiled against libweavesim_b200.so."""
+import os
+import subprocess
+
+import pytest
+
+from tests.conftest import ROOT
+
+BIN = os.path.join(ROOT, "build", "tests", "test_dropin")
+
+
+def ensure_built():
+    subprocess.run(["make", "-C", ROOT, "-s", "cpptests"], check=True, capture_output=True)
+    assert os.path.exists(BIN)
+
+
+def run(mode):
+    ensure_built()
+    p = subprocess.run([BIN, mode], capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stdout + p.stderr
+    return p.stdout
+
+
+def test_dropin_host_cases():
+    out = run("host")
+    assert "0 failed" in out
+
+
+@pytest.mark.gpu
+def test_dropin_gpu_cases():
+    out = run("gpu")
+    assert "0 failed" in out
+    print(out)
