@@ -19,9 +19,9 @@ HHDR := $(PKG)/csrc/host/tw_internal.h include/tw/tw.h
 SHIM_SRC := $(wildcard $(PKG)/csrc/host/weavesim_*.cpp)
 SHIM_HDR := $(wildcard include/weavesim/*.hpp)
 
-.PHONY: all lib shim oracle ref cpptests clean
+.PHONY: all lib shim weave oracle ref cpptests clean
 
-all: lib shim oracle cpptests
+all: lib shim weave oracle cpptests
 
 lib: $(LIBDIR)/libtw.so
 
@@ -42,6 +42,13 @@ shim: $(LIBDIR)/libweavesim_b200.so
 
 $(LIBDIR)/libweavesim_b200.so: $(SHIM_SRC) $(SHIM_HDR) $(LIBDIR)/libtw.so
 	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -o $@ $(SHIM_SRC) -L$(LIBDIR) -ltw -Wl,-rpath,'$$ORIGIN' -pthread
+
+# The weave layer runner (links cuBLAS for the synthetic GEMM load).
+weave: $(LIBDIR)/libtw_weave.so
+
+$(LIBDIR)/libtw_weave.so: $(PKG)/csrc/weave/tw_weave.cu include/tw/tw_weave.h include/tw/tw.h $(LIBDIR)/libtw.so
+	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $< -L$(LIBDIR) -ltw -lcublas -Xlinker -rpath,'$$ORIGIN' \
+	  -Xlinker -rpath,/usr/local/cuda/lib64 -Xlinker --exclude-libs,ALL
 
 # The reference's own test cases compiled against the drop-in library.
 cpptests: build/tests/test_dropin

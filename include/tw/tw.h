@@ -122,6 +122,8 @@ TW_API tw_status tw_comm_multicast_buffer(tw_comm_t comm, int rank, tw_buffer wh
  *   r'     = x + residual_shard[t-b_r]            (residual_shard overwritten, :144)
  *   out[t] = r' * rsqrt(mean(r'^2)+eps) * weight  -> OUTPUT[t] on every rank (all-gather)
  *   with TW_GATHER_RESIDUAL also r' -> RESIDUAL[t] on every rank.
+ * token_offset: the op covers rows [token_offset, token_offset+T) of the
+ *   symmetric buffers (a token split of the weave); shards are relative to it.
  * shard_ranges: 2*world int64 (must satisfy ShardMap::validate, else CONTRACT).
  * residual_shards[r]: device [e_r-b_r, H] of dtype on rank r's device.
  * weights[r]: device fp32[H] on rank r's device.  streams[r]: cudaStream_t.
@@ -130,14 +132,16 @@ TW_API tw_status tw_comm_multicast_buffer(tw_comm_t comm, int rank, tw_buffer wh
  * _group launches every rank this process owns (required when simulated ranks
  * share a device: one launch keeps them co-resident for the in-kernel
  * barrier).  Ranks never run partially: all must be launched. */
-TW_API tw_status tw_fused_allreduce_rmsnorm_group(tw_comm_t comm, int64_t T, int64_t H, const int64_t* shard_ranges,
+TW_API tw_status tw_fused_allreduce_rmsnorm_group(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset,
+                                                  const int64_t* shard_ranges,
                                            void* const* residual_shards, const float* const* weights, float eps,
                                            tw_dtype dtype, int sm_budget, unsigned flags, void* const* streams);
 
 /* --- Unfused baselines (NOT the product path) ---------------------------------
  * all_reduce (collectives.cpp:82-88) over the communicator: OUTPUT[t] = sum_r INPUT[t]
  * for every t (one-shot NVLS ld_reduce + multimem.st, or PEER loads). */
-TW_API tw_status tw_allreduce_group(tw_comm_t comm, int64_t T, int64_t H, tw_dtype dtype, int sm_budget,
+TW_API tw_status tw_allreduce_group(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset, tw_dtype dtype,
+                                    int sm_budget,
                              void* const* streams);
 
 /* --- Device memory helpers (so C/C++ hosts need no CUDA headers) ------------

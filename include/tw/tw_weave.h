@@ -1,0 +1,74 @@
+/*
+ * tw_weave.h -- C-ABI of the token-split "weave" layer runner (libtw_weave.so).
+ *
+ * Executes one transformer layer's two-stream DAG on real CUDA streams:
+ * synthetic attention / FFN GEMMs (cuBLAS -- load, not product) on a compute
+ * stream and the fused layer-boundary op (libtw.so) on a high-priority
+ * boundary stream, with a cudaEvent for every DAG edge.  The DAG shapes are
+ * the reference's (proj/src/scheduler.cpp:109-183):
+ *   TW_MODE_WEAVE      : 8 events, attn(a) -> fused(a) || attn(b) -> fused(b)
+ *                        || ffn(a) -> fused(a) || ffn(b) -> fused(b)  (:119-147)
+ *   TW_MODE_FUSE_ONLY  : attn -> fused -> ffn -> fused                 (:171-178)
+ *   TW_MODE_NO_COMM    : attn -> ffn (boundary op skipped; lower bound) (:165-169)
+ * Cross-layer edges fused(a)_L -> attn(a)_{L+1}, fused(b)_L -> attn(b)_{L+1}
+ * (:361-362) chain `layers` layers back to back.
+ *
+ * GEMM shapes are one GPU's share of the layer at tensor-parallel degree
+ * `tp` (proj/src/wavemodel.cpp:146-157,173).  The boundary op of this
+ * single-device runner is K2 (tw_rmsnorm_residual) over the split's rows --
+ * the TP=1 form of the fused op; with tp > 1 it stands in for K1, whose
+ * NVLink traffic a single GPU cannot exercise.
+ */
+#ifndef TW_TW_WEAVE_H
+#define TW_TW_WEAVE_H
+
+#include "tw/tw.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tw_layer_spec {
+  int64_t hidden;        /* H   */
+  int64_t intermediate;  /* I   */
+  int32_t heads;         /* attention heads */
+  int32_t kv_heads;
+  int32_t head_dim;
+  int32_t experts;       /* 1 = dense */
+  int32_t top_k;
+  int32_t tp;            /* GEMM shapes are per GPU at this TP degree */
+} tw_layer_spec;
+
+typedef enum tw_weave_mode {
+  TW_MODE_FUSE_ONLY = 0,
+  TW_MODE_WEAVE = 1,
+  TW_MODE_NO_COMM = 2
+} tw_weave_mode;
+
+/* Ops recorded by tw_weave_trace (the reference's OpKind, scheduler.hpp:12). */
+typedef enum tw_weave_op { TW_OP_ATTENTION = 0, TW_OP_FFN = 1, TW_OP_FUSED = 2 } tw_weave_op;
+
+typedef struct tw_weave* tw_weave_t;
+
+TW_API tw_status tw_weave_create(const tw_layer_spec* spec, int64_t max_tokens, int device, tw_weave_t* out);
+TW_API tw_status tw_weave_destroy(tw_weave_t w);
+
+/* Runs `layers` chained layers of T tokens (prefix_tokens used by WEAVE) and
+ * returns the device time per layer in microseconds (CUDA events; warm-up
+ * layer excluded).  boundary_sm_budget bounds the fused op's CTAs; when
+ * gemm_sm_target > 0 cuBLAS is asked to use that many SMs (the SM partition
+ * between compute and boundary work, scheduler.cpp:216-217). */
+TW_API tw_status tw_weave_run(tw_weave_t w, int64_t T, int64_t prefix_tokens, tw_weave_mode mode,
+                              int boundary_sm_budget, int gemm_sm_target, int layers, float* us_per_layer);
+
+/* Per-event timestamps (us from the run's start) of the LAST layer of the
+ * last tw_weave_run: op (tw_weave_op), split (0 prefix, 1 suffix, 2 whole),
+ * stream (0 compute, 1 boundary).  Arrays hold max_events entries. */
+TW_API tw_status tw_weave_trace(tw_weave_t w, int max_events, int* n_events, int* op, int* split, int* stream,
+                                float* start_us, float* end_us);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

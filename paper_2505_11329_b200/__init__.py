@@ -145,7 +145,8 @@ class Communicator:
             return torch.as_tensor(_DevBuf(self.buffer_ptr(rank, which), tuple(shape), typestr), device="cuda")
 
     def fused_allreduce_rmsnorm(self, T: int, H: int, residual_shards, weights, eps: float = 1e-5, *, dtype=None,
-                                shard_ranges=None, sm_budget: int = 8, gather_residual: bool = False, streams=None):
+                                shard_ranges=None, sm_budget: int = 8, gather_residual: bool = False, streams=None,
+                                token_offset: int = 0):
         """Kernel K1 on every rank of this communicator (see tw.h)."""
         import torch
         W = self.world
@@ -163,11 +164,11 @@ class Communicator:
             strs = (c_void_p * W)(*[_stream_handle(s) for s in streams])
         else:
             strs = (c_void_p * W)(*[torch.cuda.current_stream(d).cuda_stream for d in self.devices])
-        check(_lib.lib.tw_fused_allreduce_rmsnorm_group(self._h, T, H, ranges, res, wts, float(eps), code,
+        check(_lib.lib.tw_fused_allreduce_rmsnorm_group(self._h, T, H, token_offset, ranges, res, wts, float(eps), code,
                                                         int(sm_budget), TW_GATHER_RESIDUAL if gather_residual else 0,
                                                         strs))
 
-    def allreduce(self, T: int, H: int, dtype, *, sm_budget: int = 8, streams=None):
+    def allreduce(self, T: int, H: int, dtype, *, sm_budget: int = 8, streams=None, token_offset: int = 0):
         """Unfused AllReduce baseline (K3): OUTPUT = sum_r INPUT on every rank."""
         import torch
         W = self.world
@@ -176,7 +177,7 @@ class Communicator:
             strs = (c_void_p * W)(*[_stream_handle(s) for s in streams])
         else:
             strs = (c_void_p * W)(*[torch.cuda.current_stream(d).cuda_stream for d in self.devices])
-        check(_lib.lib.tw_allreduce_group(self._h, T, H, code, int(sm_budget), strs))
+        check(_lib.lib.tw_allreduce_group(self._h, T, H, token_offset, code, int(sm_budget), strs))
 
     def check(self) -> None:
         check(_lib.lib.tw_comm_check(self._h))

@@ -81,9 +81,9 @@ _SIGNATURES = [
     ("tw_comm_buffer", c_int, [c_void_p, c_int, c_int, POINTER(c_void_p)]),
     ("tw_comm_multicast_buffer", c_int, [c_void_p, c_int, c_int, POINTER(c_void_p)]),
     ("tw_fused_allreduce_rmsnorm_group", c_int,
-     [c_void_p, c_int64, c_int64, POINTER(c_int64), POINTER(c_void_p), POINTER(c_void_p), c_float, c_int, c_int,
+     [c_void_p, c_int64, c_int64, c_int64, POINTER(c_int64), POINTER(c_void_p), POINTER(c_void_p), c_float, c_int, c_int,
       c_uint, POINTER(c_void_p)]),
-    ("tw_allreduce_group", c_int, [c_void_p, c_int64, c_int64, c_int, c_int, POINTER(c_void_p)]),
+    ("tw_allreduce_group", c_int, [c_void_p, c_int64, c_int64, c_int64, c_int, c_int, POINTER(c_void_p)]),
     ("tw_device_alloc", c_int, [c_int, c_size_t, POINTER(c_void_p)]),
     ("tw_device_free", c_int, [c_int, c_void_p]),
     ("tw_memcpy", c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),

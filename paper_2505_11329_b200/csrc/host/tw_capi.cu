@@ -509,7 +509,7 @@ tw_status tw_comm_check(tw_comm_t comm) {
 namespace {
 
 // Common validation + launch for the fused op (K1) and the AR baseline (K3).
-tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, const int64_t* shard_ranges, void* const* residual_shards,
+tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset, const int64_t* shard_ranges, void* const* residual_shards,
                       const float* const* weights, float eps, tw_dtype dtype, int sm_budget, unsigned flags,
                       void* const* streams, bool fused) {
   const char* op = fused ? "fused_allreduce_rmsnorm" : "allreduce";
@@ -520,8 +520,9 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, const int64_t* shard
   if (dtype != TW_BF16 && dtype != TW_F32) return fail(TW_ERR_CONFIG, std::string(op) + ": unknown dtype");
   const bool bf16 = dtype == TW_BF16;
   const size_t esz = bf16 ? 2 : 4;
-  if (static_cast<size_t>(T) * static_cast<size_t>(H) * esz > comm->bytes)
-    return fail(TW_ERR_DIMENSION, std::string(op) + ": T*H exceeds the communicator buffer size");
+  if (token_offset < 0) return fail(TW_ERR_DIMENSION, std::string(op) + ": negative token offset");
+  if (static_cast<size_t>(token_offset + T) * static_cast<size_t>(H) * esz > comm->bytes)
+    return fail(TW_ERR_DIMENSION, std::string(op) + ": (token_offset+T)*H exceeds the communicator buffer size");
   int64_t local_ranges[2 * kMaxRanks];
   if (!shard_ranges) {
     tw_token_shard_map(T, W, local_ranges);
@@ -573,6 +574,7 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, const int64_t* shard
   RowParams p = {};
   p.T = T;
   p.H = H;
+  p.row_offset = token_offset;
   p.eps = eps;
   p.flags = flags;
   p.world = W;
@@ -628,16 +630,19 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, const int64_t* shard
 
 extern "C" {
 
-tw_status tw_fused_allreduce_rmsnorm_group(tw_comm_t comm, int64_t T, int64_t H, const int64_t* shard_ranges,
+tw_status tw_fused_allreduce_rmsnorm_group(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset,
+                                           const int64_t* shard_ranges,
                                            void* const* residual_shards, const float* const* weights, float eps,
                                            tw_dtype dtype, int sm_budget, unsigned flags, void* const* streams) {
   clear_error();
-  return comm_launch(comm, T, H, shard_ranges, residual_shards, weights, eps, dtype, sm_budget, flags, streams, true);
+  return comm_launch(comm, T, H, token_offset, shard_ranges, residual_shards, weights, eps, dtype, sm_budget, flags,
+                     streams, true);
 }
 
-tw_status tw_allreduce_group(tw_comm_t comm, int64_t T, int64_t H, tw_dtype dtype, int sm_budget, void* const* streams) {
+tw_status tw_allreduce_group(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset, tw_dtype dtype, int sm_budget,
+                             void* const* streams) {
   clear_error();
-  return comm_launch(comm, T, H, nullptr, nullptr, nullptr, 0.0f, dtype, sm_budget, 0u, streams, false);
+  return comm_launch(comm, T, H, token_offset, nullptr, nullptr, nullptr, 0.0f, dtype, sm_budget, 0u, streams, false);
 }
 
 }  // extern "C"

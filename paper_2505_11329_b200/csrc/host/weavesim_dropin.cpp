@@ -237,7 +237,7 @@ TokenMatrix reduce_on_device(const RankGroup& group) {
   const size_t nb = static_cast<size_t>(T * H) * sizeof(float);
   GroupContext& ctx = context_for(group.world_size, nb);
   upload_inputs(ctx, group);
-  check(tw_allreduce_group(ctx.comm, T, H, TW_F32, 8, nullptr), "all_reduce");
+  check(tw_allreduce_group(ctx.comm, T, H, 0, TW_F32, 8, nullptr), "all_reduce");
   for (int d : ctx.devices) check(tw_device_synchronize(d), "all_reduce");
   check(tw_comm_check(ctx.comm), "all_reduce");
   void* src = nullptr;
@@ -317,7 +317,7 @@ TokenMatrix fused_allreduce_rmsnorm(RankGroup& group, const NormParams& params, 
     flat.push_back(shards.ranges[r].begin);
     flat.push_back(shards.ranges[r].end);
   }
-  check(tw_fused_allreduce_rmsnorm_group(ctx.comm, T, H, flat.data(), res.data(), wts.data(), params.epsilon, TW_F32,
+  check(tw_fused_allreduce_rmsnorm_group(ctx.comm, T, H, 0, flat.data(), res.data(), wts.data(), params.epsilon, TW_F32,
                                          8, 0u, nullptr),
         "fused_allreduce_rmsnorm");
   for (int d : ctx.devices) check(tw_device_synchronize(d), "fused_allreduce_rmsnorm");

@@ -131,3 +131,84 @@ SplitPlan place_sequence_boundaries(const std::vector<std::int64_t>& sequence_le
 }
 
 }  // namespace weavesim
+
+// ---- C-ABI (include/tw/tw_split.h) ------------------------------------------------
+
+#include "tw/tw_split.h"
+
+namespace {
+
+template <class F>
+tw_status guarded(F&& f) {
+  try {
+    f();
+    return TW_OK;
+  } catch (const weavesim::DimensionError&) {
+    return TW_ERR_DIMENSION;
+  } catch (const weavesim::NumericError&) {
+    return TW_ERR_NUMERIC;
+  } catch (const weavesim::ConfigError&) {
+    return TW_ERR_CONFIG;
+  } catch (const weavesim::ContractError&) {
+    return TW_ERR_CONTRACT;
+  } catch (...) {
+    return TW_ERR_CUDA;
+  }
+}
+
+weavesim::HardwareProfile geometry(int num_sms, int tile_tokens, int cta_columns) {
+  weavesim::HardwareProfile p = weavesim::b200_geometry();
+  p.num_sms = num_sms;
+  p.tile_tokens = tile_tokens;
+  p.cta_columns = cta_columns;
+  if (p.collective_sms >= num_sms) p.collective_sms = num_sms > 1 ? num_sms - 1 : 0;
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+tw_status tw_make_split_plan(int64_t num_tokens, int num_sms, int tile_tokens, int cta_columns,
+                             int64_t threshold_tokens, int64_t* prefix, int64_t* suffix, int64_t* offset, int* mode) {
+  return guarded([&] {
+    weavesim::SplitPolicy pol;
+    pol.threshold_tokens = threshold_tokens;
+    const weavesim::SplitPlan plan =
+        weavesim::make_split_plan(num_tokens, geometry(num_sms, tile_tokens, cta_columns), pol);
+    if (prefix) *prefix = plan.prefix_tokens;
+    if (suffix) *suffix = plan.suffix_tokens;
+    if (offset) *offset = plan.offset;
+    if (mode) *mode = static_cast<int>(plan.mode);
+  });
+}
+
+tw_status tw_smart_offset_analytic(int64_t num_tokens, int num_sms, int tile_tokens, int cta_columns,
+                                   int64_t* offset) {
+  return guarded([&] {
+    *offset = weavesim::smart_offset_analytic(num_tokens, geometry(num_sms, tile_tokens, cta_columns));
+  });
+}
+
+tw_status tw_smart_offset_sweep(int64_t num_tokens, const int64_t* offset_grid, int n,
+                                double (*forward)(int64_t, int64_t, void*), void* ctx, int64_t* offset) {
+  return guarded([&] {
+    weavesim::SplitPolicy pol;
+    pol.offset_grid.assign(offset_grid, offset_grid + n);
+    *offset = weavesim::smart_offset_sweep(num_tokens, pol,
+                                           [&](std::int64_t a, std::int64_t b) { return forward(a, b, ctx); });
+  });
+}
+
+tw_status tw_place_sequence_boundaries(const int64_t* lengths, int n, int64_t total_tokens, int64_t prefix_tokens,
+                                       int64_t* prefix_len_out) {
+  return guarded([&] {
+    weavesim::SplitPlan plan;
+    plan.total_tokens = total_tokens;
+    plan.prefix_tokens = prefix_tokens;
+    plan = weavesim::place_sequence_boundaries(std::vector<std::int64_t>(lengths, lengths + n), plan);
+    std::copy(plan.prefix_len_per_sequence.begin(), plan.prefix_len_per_sequence.end(), prefix_len_out);
+  });
+}
+
+}  // extern "C"

@@ -19,7 +19,7 @@ __global__ void __launch_bounds__(kBlock, 1) allreduce_kernel(const __grid_const
   const RankSlot& s = p.slot[blockIdx.y];
   rank_barrier<X>(p, s, p.entry_target);
   const long long n = (s.end - s.begin) * p.V;  // vectors in the shard
-  const long long base = s.begin * p.H;
+  const long long base = (p.row_offset + s.begin) * p.H;
   for (long long v = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
        v += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long e = base + v * N;

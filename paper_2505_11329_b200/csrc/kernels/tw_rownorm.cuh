@@ -43,6 +43,7 @@ struct RankSlot {
 
 struct RowParams {
   long long T, H;
+  long long row_offset;  // K1: first token row of the symmetric buffers this op covers
   int V;    // vectors per row (H / N)
   int tpr;  // threads per row group (multiple of 32)
   float eps;
@@ -251,7 +252,7 @@ __global__ void __launch_bounds__(kBlock, 1) rownorm_kernel(const __grid_constan
   int parity = 0;
   for (long long t = row0 + static_cast<long long>(blockIdx.x) * groups + group; t < row1;
        t += stride, parity ^= 1) {
-    const long long rowe = t * H;  // element offset of the row in [T,H] buffers
+    const long long rowe = (X == Xport::Local ? t : p.row_offset + t) * H;  // row in the [T,H] buffers
     const long long srow = (X == Xport::Local) ? rowe : (t - row0) * H;  // residual row
     const void* res_src = (X == Xport::Local) ? p.res_in : s.residual;
     void* res_dst = (X == Xport::Local) ? p.res_out : s.residual;

@@ -1,0 +1,429 @@
+// tw_weave.cu -- the token-split weave as real CUDA streams (libtw_weave.so).
+//
+// The reference builds this DAG only to price it in a simulator
+// (proj/src/scheduler.cpp:109-183, simulate :185-299).  Here every node is a
+// real launch: cuBLAS bf16 GEMMs for the synthetic attention / FFN load on the
+// compute stream (library work, not the product) and the fused boundary op
+// from libtw.so on a highest-priority stream; every DAG edge is a cudaEvent.
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tw/tw.h"
+#include "tw/tw_weave.h"
+
+namespace {
+
+thread_local char g_err[512];
+
+tw_status werr(tw_status st, const std::string& msg) {
+  std::snprintf(g_err, sizeof(g_err), "%s", msg.c_str());
+  std::fprintf(stderr, "tw_weave: %s\n", g_err);
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                             \
+  do {                                                                             \
+    cudaError_t e_ = (expr);                                                       \
+    if (e_ != cudaSuccess) return werr(TW_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+#define CUBLAS_TRY(expr)                                                           \
+  do {                                                                             \
+    cublasStatus_t s_ = (expr);                                                    \
+    if (s_ != CUBLAS_STATUS_SUCCESS) return werr(TW_ERR_CUDA, std::string(#expr) + ": cublas status " + std::to_string(s_)); \
+  } while (0)
+
+#define TW_TRY(expr)                                                               \
+  do {                                                                             \
+    tw_status t_ = (expr);                                                         \
+    if (t_ != TW_OK) return werr(t_, std::string(#expr) + ": " + tw_last_error()); \
+  } while (0)
+
+struct Ev {
+  int op, split, stream;
+  cudaEvent_t start, end;
+};
+
+}  // namespace
+
+struct tw_weave {
+  tw_layer_spec spec;
+  int64_t max_tokens = 0;
+  int device = 0;
+  cublasHandle_t blas = nullptr;
+  cudaStream_t compute = nullptr, boundary = nullptr;
+  // activations (bf16)
+  void *X = nullptr, *P = nullptr, *R = nullptr, *QKV = nullptr, *S = nullptr, *A = nullptr, *F = nullptr,
+       *PE = nullptr;
+  // weights (bf16) + norm weight (fp32)
+  void *Wqkv = nullptr, *Wo = nullptr, *Wup = nullptr, *Wdown = nullptr;
+  float* wnorm = nullptr;
+  int64_t qkvw = 0, hg = 0, ffn_w = 0, moe_rows = 0;
+  std::vector<Ev> pool;
+  size_t pool_used = 0;
+  std::vector<size_t> last_layer_events;
+  cudaEvent_t t0 = nullptr;
+  std::vector<cudaEvent_t> dag;  // edge events
+  size_t dag_used = 0;
+};
+
+namespace {
+
+constexpr size_t kBf16 = 2;
+
+// Row-major C[M,N] = A[M,K] * B[K,N] (bf16 in, fp32 accumulate), batched.
+cublasStatus_t gemm_rm(cublasHandle_t h, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int64_t sA,
+                       const void* B, int64_t ldb, int64_t sB, void* C, int64_t ldc, int64_t sC, int batch) {
+  if (M <= 0 || N <= 0 || K <= 0 || batch <= 0) return CUBLAS_STATUS_SUCCESS;
+  const float alpha = 1.0f, beta = 0.0f;
+  return cublasGemmStridedBatchedEx(h, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(N), static_cast<int>(M),
+                                    static_cast<int>(K), &alpha, B, CUDA_R_16BF, static_cast<int>(ldb), sB, A,
+                                    CUDA_R_16BF, static_cast<int>(lda), sA, &beta, C, CUDA_R_16BF,
+                                    static_cast<int>(ldc), sC, batch, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
+}
+
+cudaEvent_t edge(tw_weave* w) {
+  if (w->dag_used == w->dag.size()) {
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    w->dag.push_back(e);
+  }
+  return w->dag[w->dag_used++];
+}
+
+size_t op_begin(tw_weave* w, int op, int split, int stream_id, cudaStream_t s) {
+  if (w->pool_used == w->pool.size()) {
+    Ev e{};
+    cudaEventCreate(&e.start);
+    cudaEventCreate(&e.end);
+    w->pool.push_back(e);
+  }
+  Ev& e = w->pool[w->pool_used];
+  e.op = op;
+  e.split = split;
+  e.stream = stream_id;
+  cudaEventRecord(e.start, s);
+  return w->pool_used++;
+}
+
+void op_end(tw_weave* w, size_t id, cudaStream_t s) { cudaEventRecord(w->pool[id].end, s); }
+
+// ---- layer ops -------------------------------------------------------------------
+
+// Attention for query rows [r0, r0+n) with kv_prior earlier context tokens:
+// QKV projection, the causal attention core as two batched GEMMs over the
+// heads of this GPU with L = kv_prior + n/2 keys (flops = 4*h*d*(n^2/2 +
+// n*kv_prior), proj/src/wavemodel.cpp:150-153), and the O projection into
+// the partial-sum buffer P (the tensor the boundary op all-reduces).
+tw_status attention(tw_weave* w, int64_t r0, int64_t n, int64_t kv_prior) {
+  if (n <= 0) return TW_OK;
+  const tw_layer_spec& sp = w->spec;
+  const int64_t H = sp.hidden, d = sp.head_dim;
+  const int64_t L = std::max<int64_t>(1, kv_prior + n / 2);
+  char* X = static_cast<char*>(w->X);
+  char* QKV = static_cast<char*>(w->QKV);
+  char* A = static_cast<char*>(w->A);
+  char* P = static_cast<char*>(w->P);
+  CUBLAS_TRY(gemm_rm(w->blas, n, w->qkvw, H, X + r0 * H * kBf16, H, 0, w->Wqkv, w->qkvw, 0,
+                     QKV + r0 * w->qkvw * kBf16, w->qkvw, 0, 1));
+  // scores[h] = Q_h [n x d] * K_h^T [d x L]   (K_h read as a [d x L] operand)
+  CUBLAS_TRY(gemm_rm(w->blas, n, L, d, QKV + r0 * w->qkvw * kBf16, w->qkvw, d, QKV, L, d * L, w->S, L, n * L,
+                     static_cast<int>(w->hg)));
+  // out[h] = scores[h] [n x L] * V_h [L x d]
+  CUBLAS_TRY(gemm_rm(w->blas, n, d, L, w->S, L, n * L, QKV, d, L * d, A + r0 * (w->hg * d) * kBf16, w->hg * d, d,
+                     static_cast<int>(w->hg)));
+  CUBLAS_TRY(gemm_rm(w->blas, n, H, w->hg * d, A + r0 * (w->hg * d) * kBf16, w->hg * d, 0, w->Wo, H, 0,
+                     P + r0 * H * kBf16, H, 0, 1));
+  return TW_OK;
+}
+
+// FFN for rows [r0, r0+n): gate+up [H -> 2I/tp] and down [I/tp -> H] into P.
+// MoE: T*top_k/E rows per expert, one batched GEMM pair over the experts
+// (uniform routing, proj/src/wavemodel.cpp:169-186).
+tw_status ffn(tw_weave* w, int64_t r0, int64_t n) {
+  if (n <= 0) return TW_OK;
+  const tw_layer_spec& sp = w->spec;
+  const int64_t H = sp.hidden, I = sp.intermediate / sp.tp;
+  char* X = static_cast<char*>(w->X);
+  char* F = static_cast<char*>(w->F);
+  char* P = static_cast<char*>(w->P);
+  if (sp.experts <= 1) {
+    CUBLAS_TRY(gemm_rm(w->blas, n, 2 * I, H, X + r0 * H * kBf16, H, 0, w->Wup, 2 * I, 0, F + r0 * 2 * I * kBf16,
+                       2 * I, 0, 1));
+    CUBLAS_TRY(gemm_rm(w->blas, n, H, I, F + r0 * 2 * I * kBf16, 2 * I, 0, w->Wdown, H, 0, P + r0 * H * kBf16, H, 0,
+                       1));
+    return TW_OK;
+  }
+  const int64_t rows = (n * sp.top_k + sp.experts - 1) / sp.experts;
+  CUBLAS_TRY(gemm_rm(w->blas, rows, 2 * I, H, X + r0 * H * kBf16, H, 0, w->Wup, 2 * I, H * 2 * I, F, 2 * I,
+                     rows * 2 * I, sp.experts));
+  CUBLAS_TRY(gemm_rm(w->blas, rows, H, I, F, 2 * I, rows * 2 * I, w->Wdown, H, I * H, w->PE, H, rows * H,
+                     sp.experts));
+  return TW_OK;
+}
+
+// Layer-boundary op on rows [r0, r0+n): K2 (tp == 1) reading the partial sums
+// P, updating the residual R in place and writing the normed hidden X.
+tw_status fused(tw_weave* w, int64_t r0, int64_t n, int budget, cudaStream_t s) {
+  if (n <= 0) return TW_OK;
+  const int64_t H = w->spec.hidden;
+  char* P = static_cast<char*>(w->P);
+  char* R = static_cast<char*>(w->R);
+  char* X = static_cast<char*>(w->X);
+  TW_TRY(tw_rmsnorm_residual(P + r0 * H * kBf16, R + r0 * H * kBf16, R + r0 * H * kBf16, X + r0 * H * kBf16,
+                             w->wnorm, n, H, 1e-5f, TW_BF16, budget, s));
+  return TW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tw_status tw_weave_create(const tw_layer_spec* spec, int64_t max_tokens, int device, tw_weave_t* out) {
+  if (!spec || !out) return werr(TW_ERR_CONFIG, "weave_create: null argument");
+  *out = nullptr;
+  const tw_layer_spec& sp = *spec;
+  if (sp.hidden < 1 || sp.intermediate < 1 || sp.heads < 1 || sp.kv_heads < 1 || sp.head_dim < 1 ||
+      sp.heads % sp.kv_heads || sp.experts < 1 || sp.top_k < 1 || sp.top_k > sp.experts || sp.tp < 1 ||
+      sp.heads % sp.tp || sp.intermediate % sp.tp || max_tokens < 1)
+    return werr(TW_ERR_CONFIG, "weave_create: invalid layer spec (LayerSpec::validate, wavemodel.cpp:23-36)");
+  CUDA_TRY(cudaSetDevice(device));
+  auto* w = new tw_weave();
+  w->spec = sp;
+  w->max_tokens = max_tokens;
+  w->device = device;
+  const int64_t H = sp.hidden, T = max_tokens, d = sp.head_dim, I = sp.intermediate / sp.tp;
+  w->hg = sp.heads / sp.tp;
+  w->qkvw = (H + 2 * sp.kv_heads * d) / sp.tp;
+  const int64_t hd = w->hg * d;
+  w->moe_rows = (T * sp.top_k + sp.experts - 1) / sp.experts;
+  const int64_t frows = sp.experts > 1 ? w->moe_rows * sp.experts : T;
+  struct Alloc {
+    void** p;
+    size_t bytes;
+  } allocs[] = {
+      {&w->X, size_t(T * H * kBf16)},
+      {&w->P, size_t(T * H * kBf16)},
+      {&w->R, size_t(T * H * kBf16)},
+      {&w->QKV, size_t(T * std::max(w->qkvw, hd) * kBf16) + size_t(T * d * kBf16)},
+      {&w->S, size_t(w->hg * T * T * kBf16)},
+      {&w->A, size_t(T * hd * kBf16)},
+      {&w->F, size_t(frows * 2 * I * kBf16)},
+      {&w->PE, size_t(sp.experts > 1 ? frows * H * kBf16 : 16)},
+      {&w->Wqkv, size_t(H * w->qkvw * kBf16)},
+      {&w->Wo, size_t(hd * H * kBf16)},
+      {&w->Wup, size_t(sp.experts * H * 2 * I * kBf16)},
+      {&w->Wdown, size_t(sp.experts * I * H * kBf16)},
+      {reinterpret_cast<void**>(&w->wnorm), size_t(H * sizeof(float))},
+  };
+  for (const Alloc& a : allocs) {
+    cudaError_t e = cudaMalloc(a.p, a.bytes);
+    if (e == cudaSuccess) e = cudaMemset(*a.p, 0, a.bytes);
+    if (e != cudaSuccess) {
+      tw_weave_destroy(w);
+      return werr(TW_ERR_CUDA, std::string("weave_create: cudaMalloc: ") + cudaGetErrorString(e));
+    }
+  }
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  CUDA_TRY(cudaStreamCreateWithPriority(&w->compute, cudaStreamNonBlocking, lo));
+  CUDA_TRY(cudaStreamCreateWithPriority(&w->boundary, cudaStreamNonBlocking, hi));
+  CUBLAS_TRY(cublasCreate(&w->blas));
+  CUBLAS_TRY(cublasSetStream(w->blas, w->compute));
+  CUDA_TRY(cudaEventCreate(&w->t0));
+  *out = w;
+  return TW_OK;
+}
+
+tw_status tw_weave_destroy(tw_weave_t w) {
+  if (!w) return TW_OK;
+  cudaSetDevice(w->device);
+  cudaDeviceSynchronize();
+  void* bufs[] = {w->X, w->P, w->R, w->QKV, w->S, w->A, w->F, w->PE, w->Wqkv, w->Wo, w->Wup, w->Wdown, w->wnorm};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  for (Ev& e : w->pool) {
+    cudaEventDestroy(e.start);
+    cudaEventDestroy(e.end);
+  }
+  for (cudaEvent_t e : w->dag) cudaEventDestroy(e);
+  if (w->t0) cudaEventDestroy(w->t0);
+  if (w->blas) cublasDestroy(w->blas);
+  if (w->compute) cudaStreamDestroy(w->compute);
+  if (w->boundary) cudaStreamDestroy(w->boundary);
+  delete w;
+  return TW_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+// One layer's DAG.  carry_a / carry_b: the previous layer's last boundary
+// events for the prefix / suffix (cross-layer edges, scheduler.cpp:361-362);
+// updated on return.  Records per-op timing events into the pool.
+tw_status layer(tw_weave* w, int64_t T, int64_t ta, tw_weave_mode mode, int budget, cudaEvent_t& carry_a,
+                cudaEvent_t& carry_b) {
+  cudaStream_t cs = w->compute, bs = w->boundary;
+  if (mode != TW_MODE_WEAVE) {
+    // Sequential chain on one stream: attn -> fused -> ffn -> fused.
+    if (carry_a) CUDA_TRY(cudaStreamWaitEvent(cs, carry_a, 0));
+    size_t id = op_begin(w, TW_OP_ATTENTION, 2, 0, cs);
+    TW_TRY(attention(w, 0, T, 0));
+    op_end(w, id, cs);
+    if (mode == TW_MODE_FUSE_ONLY) {
+      id = op_begin(w, TW_OP_FUSED, 2, 0, cs);
+      TW_TRY(fused(w, 0, T, 0, cs));
+      op_end(w, id, cs);
+    }
+    id = op_begin(w, TW_OP_FFN, 2, 0, cs);
+    TW_TRY(ffn(w, 0, T));
+    op_end(w, id, cs);
+    if (mode == TW_MODE_FUSE_ONLY) {
+      id = op_begin(w, TW_OP_FUSED, 2, 0, cs);
+      TW_TRY(fused(w, 0, T, 0, cs));
+      op_end(w, id, cs);
+    }
+    carry_a = edge(w);
+    CUDA_TRY(cudaEventRecord(carry_a, cs));
+    carry_b = nullptr;
+    return TW_OK;
+  }
+  const int64_t tb = T - ta;
+  // compute: attn(a)
+  if (carry_a) CUDA_TRY(cudaStreamWaitEvent(cs, carry_a, 0));
+  size_t id = op_begin(w, TW_OP_ATTENTION, 0, 0, cs);
+  TW_TRY(attention(w, 0, ta, 0));
+  op_end(w, id, cs);
+  cudaEvent_t e_aa = edge(w);
+  CUDA_TRY(cudaEventRecord(e_aa, cs));
+  // boundary: fused(a) after attn(a)
+  CUDA_TRY(cudaStreamWaitEvent(bs, e_aa, 0));
+  id = op_begin(w, TW_OP_FUSED, 0, 1, bs);
+  TW_TRY(fused(w, 0, ta, budget, bs));
+  op_end(w, id, bs);
+  cudaEvent_t e_fa1 = edge(w);
+  CUDA_TRY(cudaEventRecord(e_fa1, bs));
+  // compute: attn(b) -- chunked-attention edge: keys include the prefix
+  if (carry_b) CUDA_TRY(cudaStreamWaitEvent(cs, carry_b, 0));
+  id = op_begin(w, TW_OP_ATTENTION, 1, 0, cs);
+  TW_TRY(attention(w, ta, tb, ta));
+  op_end(w, id, cs);
+  cudaEvent_t e_ab = edge(w);
+  CUDA_TRY(cudaEventRecord(e_ab, cs));
+  // boundary: fused(b) after attn(b) (and fused(a): same stream)
+  CUDA_TRY(cudaStreamWaitEvent(bs, e_ab, 0));
+  id = op_begin(w, TW_OP_FUSED, 1, 1, bs);
+  TW_TRY(fused(w, ta, tb, budget, bs));
+  op_end(w, id, bs);
+  cudaEvent_t e_fb1 = edge(w);
+  CUDA_TRY(cudaEventRecord(e_fb1, bs));
+  // compute: ffn(a) after fused(a)
+  CUDA_TRY(cudaStreamWaitEvent(cs, e_fa1, 0));
+  id = op_begin(w, TW_OP_FFN, 0, 0, cs);
+  TW_TRY(ffn(w, 0, ta));
+  op_end(w, id, cs);
+  cudaEvent_t e_ffa = edge(w);
+  CUDA_TRY(cudaEventRecord(e_ffa, cs));
+  // boundary: fused(a) after ffn(a), fused(b)
+  CUDA_TRY(cudaStreamWaitEvent(bs, e_ffa, 0));
+  id = op_begin(w, TW_OP_FUSED, 0, 1, bs);
+  TW_TRY(fused(w, 0, ta, budget, bs));
+  op_end(w, id, bs);
+  carry_a = edge(w);
+  CUDA_TRY(cudaEventRecord(carry_a, bs));
+  // compute: ffn(b) after fused(b)
+  CUDA_TRY(cudaStreamWaitEvent(cs, e_fb1, 0));
+  id = op_begin(w, TW_OP_FFN, 1, 0, cs);
+  TW_TRY(ffn(w, ta, tb));
+  op_end(w, id, cs);
+  cudaEvent_t e_ffb = edge(w);
+  CUDA_TRY(cudaEventRecord(e_ffb, cs));
+  // boundary: fused(b) after ffn(b), fused(a)
+  CUDA_TRY(cudaStreamWaitEvent(bs, e_ffb, 0));
+  id = op_begin(w, TW_OP_FUSED, 1, 1, bs);
+  TW_TRY(fused(w, ta, tb, budget, bs));
+  op_end(w, id, bs);
+  carry_b = edge(w);
+  CUDA_TRY(cudaEventRecord(carry_b, bs));
+  return TW_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+tw_status tw_weave_run(tw_weave_t w, int64_t T, int64_t prefix_tokens, tw_weave_mode mode, int boundary_sm_budget,
+                       int gemm_sm_target, int layers, float* us_per_layer) {
+  if (!w || !us_per_layer) return werr(TW_ERR_CONFIG, "weave_run: null argument");
+  if (T < 1 || T > w->max_tokens) return werr(TW_ERR_DIMENSION, "weave_run: T out of range");
+  if (layers < 1) return werr(TW_ERR_CONFIG, "weave_run: layers must be >= 1");
+  if (mode == TW_MODE_WEAVE && (prefix_tokens < 1 || prefix_tokens >= T))
+    return werr(TW_ERR_CONTRACT, "weave_run: TokenWeave requires an Overlap split (0 < prefix < T), "
+                                 "scheduler.cpp:116-118");
+  CUDA_TRY(cudaSetDevice(w->device));
+  CUBLAS_TRY(cublasSetSmCountTarget(w->blas, mode == TW_MODE_WEAVE ? std::max(0, gemm_sm_target) : 0));
+  cudaEvent_t ca = nullptr, cb = nullptr;
+  // warm-up layer (cuBLAS heuristics, first-launch costs), not timed
+  w->pool_used = 0;
+  w->dag_used = 0;
+  tw_status st = layer(w, T, prefix_tokens, mode, boundary_sm_budget, ca, cb);
+  if (st != TW_OK) return st;
+  CUDA_TRY(cudaStreamSynchronize(w->compute));
+  CUDA_TRY(cudaStreamSynchronize(w->boundary));
+  w->pool_used = 0;
+  w->dag_used = 0;
+  ca = cb = nullptr;
+  CUDA_TRY(cudaEventRecord(w->t0, w->compute));
+  CUDA_TRY(cudaStreamWaitEvent(w->boundary, w->t0, 0));
+  size_t last_begin = 0;
+  for (int l = 0; l < layers; ++l) {
+    last_begin = w->pool_used;
+    st = layer(w, T, prefix_tokens, mode, boundary_sm_budget, ca, cb);
+    if (st != TW_OK) return st;
+  }
+  // join both streams onto compute, then stop the clock
+  if (cb) CUDA_TRY(cudaStreamWaitEvent(w->compute, cb, 0));
+  if (ca) CUDA_TRY(cudaStreamWaitEvent(w->compute, ca, 0));
+  cudaEvent_t t1 = edge(w);
+  cudaEvent_t t1t;
+  CUDA_TRY(cudaEventCreate(&t1t));
+  (void)t1;
+  CUDA_TRY(cudaEventRecord(t1t, w->compute));
+  CUDA_TRY(cudaEventSynchronize(t1t));
+  float ms = 0;
+  CUDA_TRY(cudaEventElapsedTime(&ms, w->t0, t1t));
+  cudaEventDestroy(t1t);
+  *us_per_layer = 1000.0f * ms / layers;
+  w->last_layer_events.clear();
+  for (size_t i = last_begin; i < w->pool_used; ++i) w->last_layer_events.push_back(i);
+  CUBLAS_TRY(cublasSetSmCountTarget(w->blas, 0));
+  return TW_OK;
+}
+
+tw_status tw_weave_trace(tw_weave_t w, int max_events, int* n_events, int* op, int* split, int* stream,
+                         float* start_us, float* end_us) {
+  if (!w || !n_events) return werr(TW_ERR_CONFIG, "weave_trace: null argument");
+  const int n = static_cast<int>(std::min<size_t>(w->last_layer_events.size(), std::max(0, max_events)));
+  *n_events = n;
+  for (int i = 0; i < n; ++i) {
+    const Ev& e = w->pool[w->last_layer_events[i]];
+    float a = 0, b = 0;
+    CUDA_TRY(cudaEventElapsedTime(&a, w->t0, e.start));
+    CUDA_TRY(cudaEventElapsedTime(&b, w->t0, e.end));
+    if (op) op[i] = e.op;
+    if (split) split[i] = e.split;
+    if (stream) stream[i] = e.stream;
+    if (start_us) start_us[i] = 1000.0f * a;
+    if (end_us) end_us[i] = 1000.0f * b;
+  }
+  return TW_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,121 @@
+"""The weave: split planner parity (CPU) and the two-stream layer runner (GPU)."""
+import pytest
+
+
+def test_planner_matches_golden_plans(golden):
+    from paper_2505_11329_b200 import weave
+    meta, _ = golden
+    for p in meta["plans"]:
+        got = weave.make_split_plan(p["T"], p["num_sms"], p["tile_tokens"], p["cta_columns"], p["threshold"])
+        assert got == (p["prefix"], p["suffix"], p["offset"], p["mode"]), p
+
+
+def test_planner_matches_oracle_everywhere(orc):
+    from paper_2505_11329_b200 import weave
+    for T in list(range(0, 20000, 61)) + [4096, 6144, 9600]:
+        for sms, tile, cols in ((148, 128, 32), (132, 128, 32), (132, 128, 4), (148, 64, 8)):
+            assert weave.smart_offset_analytic(T, sms, tile, cols) == orc.smart_offset_analytic(T, sms, tile, cols)
+            for thr in (1024, 4096):
+                assert weave.make_split_plan(T, sms, tile, cols, thr) == orc.make_split_plan(T, thr, sms, tile, cols)
+
+
+def test_planner_matches_reference_directly(ref):
+    from paper_2505_11329_b200 import weave
+    for T in range(0, 40000, 173):
+        assert weave.smart_offset_analytic(T) == ref.smart_offset_analytic(T, 148, 128, 32)
+
+
+def test_sweep_and_sequence_cut(orc):
+    from paper_2505_11329_b200 import weave
+    # Alg. 1 tie rules (proj/tests/test_splitter.cpp:83-101)
+    assert weave.smart_offset_sweep(4096, lambda a, b: 1.0) == 0
+    assert weave.smart_offset_sweep(4096, lambda a, b: 0.5 if a == 2048 + 192 else 1.0) == 192
+    assert weave.smart_offset_sweep(100, lambda a, b: -a) == 0  # offsets >= T/2 skipped
+    assert weave.place_sequence_boundaries([30, 40, 30], 100, 55) == [30, 25, 0]
+    assert weave.place_sequence_boundaries([30, 40, 30], 100, 55) == orc.place_sequence_boundaries([30, 40, 30],
+                                                                                                    100, 55)
+    import paper_2505_11329_b200 as tw
+    with pytest.raises(tw.ContractError):
+        weave.place_sequence_boundaries([30, 40], 100, 55)
+    with pytest.raises(tw.ConfigError):
+        weave.make_split_plan(4096, threshold=0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("model", ["llama-70b", "mixtral-8x22b"])
+def test_layer_runner_modes_and_dag(cuda, model):
+    from paper_2505_11329_b200 import weave
+    T = 2048
+    r = weave.LayerRunner(model, tp=8, max_tokens=T)
+    prefix = T // 2 + 128
+    seq = r.run(T, "fuseonly", layers=3)
+    tr_seq = r.trace()
+    nocomm = r.run(T, "nocomm", layers=3)
+    tw_ = r.run(T, "tokenweave", prefix=prefix, boundary_sms=16, layers=3)
+    tr = r.trace()
+    assert seq > 0 and nocomm > 0 and tw_ > 0
+    assert nocomm <= seq * 1.05  # the boundary op only adds work
+    # reference DAG shapes (proj/tests/test_scheduler.cpp:108-136)
+    assert len(tr_seq) == 4 and sum(e["op"] == "fused_ar_norm" for e in tr_seq) == 2
+    assert len(tr) == 8 and sum(e["op"] == "fused_ar_norm" and e["stream"] == "comm" for e in tr) == 4
+    ev = {(e["op"], e["split"], i): e for i, e in enumerate(tr)}
+    order = [(e["op"], e["split"]) for e in tr]
+    assert order == [("attention", "prefix"), ("fused_ar_norm", "prefix"), ("attention", "suffix"),
+                     ("fused_ar_norm", "suffix"), ("ffn", "prefix"), ("fused_ar_norm", "prefix"), ("ffn", "suffix"),
+                     ("fused_ar_norm", "suffix")]
+    eps = 2.0  # us of event-timestamp slack
+    aa, fa1, ab, fb1, ffa, fa2, ffb, fb2 = tr
+    assert fa1["start_us"] >= aa["end_us"] - eps          # fa1 <- aa
+    assert ab["start_us"] >= aa["end_us"] - eps           # chunked-attention edge
+    assert fb1["start_us"] >= max(ab["end_us"], fa1["end_us"]) - eps
+    assert ffa["start_us"] >= fa1["end_us"] - eps
+    assert fa2["start_us"] >= max(ffa["end_us"], fb1["end_us"]) - eps
+    assert ffb["start_us"] >= fb1["end_us"] - eps
+    assert fb2["start_us"] >= max(ffb["end_us"], fa2["end_us"]) - eps
+    r.close()
+
+
+@pytest.mark.gpu
+def test_weave_contract_errors(cuda):
+    import paper_2505_11329_b200 as tw
+    from paper_2505_11329_b200 import weave
+    r = weave.LayerRunner("llama-70b", tp=8, max_tokens=1024)
+    with pytest.raises(tw.ContractError):
+        r.run(1024, "tokenweave", prefix=0)
+    with pytest.raises(tw.DimensionError):
+        r.run(4096, "fuseonly")
+    r.close()
+
+
+@pytest.mark.gpu
+def test_k1_token_offset_split_ops(cuda, orc):
+    """A weave split runs K1 on rows [a, b) of the symmetric buffers: two split
+    ops must equal the one whole-batch op."""
+    import numpy as np
+    import torch
+    import paper_2505_11329_b200 as tw
+    from tests.helpers import assert_bf16_close, bf16_round, group_inputs
+    W, T, H = 4, 300, 1024
+    ta = 172
+    inputs, residual, weight = group_inputs(3, W, T, H)
+    inputs, residual = bf16_round(inputs), bf16_round(residual)
+    comm = tw.Communicator(W, [0] * W, T * H * 2, tw.TW_TRANSPORT_PEER)
+    for r in range(W):
+        comm.buffer(r, 0, (T, H), torch.bfloat16).copy_(torch.from_numpy(inputs[r]).bfloat16())
+    wts = [torch.from_numpy(weight).cuda()] * W
+    shards_all = []
+    for (a, b) in ((0, ta), (ta, T)):
+        n = b - a
+        ranges = tw.token_shard_map(n, W)
+        shards = [torch.from_numpy(np.ascontiguousarray(residual[a + s:a + e])).cuda().bfloat16()
+                  for s, e in ranges]
+        comm.fused_allreduce_rmsnorm(n, H, shards, wts, token_offset=a, sm_budget=4)
+        shards_all.append(torch.cat(shards))
+    torch.cuda.synchronize()
+    comm.check()
+    want_out, want_res = orc.fused_allreduce_rmsnorm(list(inputs), [residual[b:e] for b, e in
+                                                                    orc.token_shard_map(T, W)], weight)
+    for r in range(W):
+        assert_bf16_close(comm.buffer(r, 1, (T, H), torch.bfloat16).float().cpu().numpy(), want_out)
+    assert np.array_equal(torch.cat(shards_all).float().cpu().numpy(), bf16_round(np.concatenate(want_res)))
+    comm.close()
