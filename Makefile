@@ -14,6 +14,7 @@ OBJDIR := build/obj
 
 KSRC := $(PKG)/csrc/kernels/tw_launch.cu
 HSRC := $(PKG)/csrc/host/tw_capi.cu
+MPSRC := $(PKG)/csrc/host/tw_mp.cu
 KHDR := $(wildcard $(PKG)/csrc/kernels/*.cuh) $(PKG)/csrc/kernels/tw_launch.h
 HHDR := $(PKG)/csrc/host/tw_internal.h include/tw/tw.h
 SHIM_SRC := $(wildcard $(PKG)/csrc/host/weavesim_*.cpp)
@@ -33,7 +34,11 @@ $(OBJDIR)/tw_capi.o: $(HSRC) $(HHDR) $(KHDR)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(LIBDIR)/libtw.so: $(OBJDIR)/tw_launch.o $(OBJDIR)/tw_capi.o
+$(OBJDIR)/tw_mp.o: $(MPSRC) $(HHDR) $(KHDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIBDIR)/libtw.so: $(OBJDIR)/tw_launch.o $(OBJDIR)/tw_capi.o $(OBJDIR)/tw_mp.o
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -Xlinker --exclude-libs,ALL
 

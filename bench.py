@@ -1,22 +1,23 @@
 #!/usr/bin/env python3
 """bench.py -- the fused AR + residual-add + RMSNorm hot path on B200.
 
-Contract:
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N=1 workload: BASELINE.json configs[2] at TP=1 -- the Qwen2.5-72B / Llama
-layer-boundary shape 8192 tokens x 8192 hidden bf16 (configs[1], TP=8 on
-8xB200, does not fit one GPU).  At TP=1 the fused op degenerates to kernel K2
-(fused residual-add + RMSNorm, HBM-bound).  A "step" is one fused op over one
-[T,H] batch.  `value` = device time per op (CUDA events on the launching
-stream, max over ranks), microseconds, lower is better.
+N=1 workload: BASELINE.json configs[2] at TP=1 -- the Qwen2.5-72B /
+Llama-3.3-70B layer-boundary shape, 8192 tokens x 8192 hidden, bf16
+(configs[1] is TP=8 on 8xB200 and does not fit one GPU).  At TP=1 the fused
+op degenerates to kernel K2 (fused residual-add + RMSNorm, HBM-bound).  A
+"step" is one fused op over one [T,H] batch; `value` = device time per op
+(CUDA events on the launching stream, max over ranks), microseconds, lower is
+better.  `e2e` is the same op through the C-ABI with pinned HOST buffers
+(H2D of input+residual and D2H of output+residual inside the timed region).
 
 N>1 (torchrun, one process per GPU): TP=N fused AllReduce + residual + RMSNorm
-(kernel K1) over the multi-process communicator, strong scaling (same T).
+(kernel K1) over the multi-process NVLS communicator (tools/bench_tp.py).
 
 --impl reference: the reference's own CPU implementation of the path
-(oracle/_ref = proj/src/numerics.cpp + collectives.cpp compiled unmodified)
-on the host cores, same config/metric.
+(oracle/_ref = proj/src/numerics.cpp compiled unmodified) on the host cores,
+same config / metric / unit.
 """
 from __future__ import annotations
 
@@ -34,26 +35,37 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fused AR+RMSNorm µs & NVLink GB/s, 1024–8192 tok × 8192 hid, TP=1/2/4/8"
 UNIT = "us"
-T_DEFAULT = 8192
-H_DEFAULT = 8192
 EPS = 1e-5
+FLUSH_NOTE = ("L2 flushed between steps outside the event pair: 256 MiB buffer written then read back "
+              "(> 126 MB L2; leaves clean lines, none of the op's inputs); working set 512 MiB > L2")
 
 
-def measured_peaks():
+def measured_hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            p = json.load(f)
-        return float(p["hbm_gbs"]), "measured"
+            return float(json.load(f)["hbm_gbs"]), "measured copy bandwidth (MEASURED_PEAKS.json)"
     except Exception:
-        return 6650.0, "fallback"
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class L2Flush:
+    def __init__(self, device):
+        import torch
+        self.buf = torch.empty(256 << 20, dtype=torch.uint8, device=device)
+        self.sink = torch.empty(1, dtype=torch.float32, device=device)
+
+    def __call__(self, i: int):
+        self.buf.fill_(i & 0x7F)
+        self.sink.copy_(self.buf.view(-1).view(__import__("torch").float32).sum().reshape(1))
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi SM clocks + throttle reasons sampled during the timed region."""
 
     FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int = 0):
         self.index = index
@@ -97,147 +109,86 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower().startswith("active")})
-        loaded = [x for x in sm if x > 0.5 * (max(mx) if mx else 0)] or sm
-        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+        num = lambda s: s.replace(".", "", 1).isdigit()  # noqa: E731
+        sm = [float(s[0]) for s in self.samples if num(s[0])]
+        mx = [float(s[1]) for s in self.samples if num(s[1])]
+        reasons = sorted({self.NAMES[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        top = max(mx) if mx else 0.0
+        loaded = [x for x in sm if x > 0.5 * top] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": top or None,
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def cpu_reference_times(T, H, steps, threads):
-    """The reference rmsnorm_residual (oracle/_ref) timed on the host cores."""
-    import oracle  # cpu_baseline leg only
-    ref = oracle.RefLib()
-    return [ref.time_rmsnorm(T, H, threads, 1) for _ in range(steps)]
+# ---- reference CPU arm ----------------------------------------------------------------
+
+def reference_rmsnorm_ms(T, H, threads, iters):
+    """weavesim::rmsnorm_residual (oracle/_ref, the reference sources compiled
+    unmodified), token rows chunked over `threads` host threads."""
+    import oracle  # cpu_baseline / --impl reference legs only
+    return oracle.RefLib().time_rmsnorm(T, H, threads, iters)
 
 
 def run_reference_arm(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
     T, H = args.tokens, args.hidden
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
-        cpu_reference_times(T, H, 1, threads)
+        reference_rmsnorm_ms(T, H, threads, 1)
     t0 = time.perf_counter()
-    ms = cpu_reference_times(T, H, args.steps, threads)
+    ms = [reference_rmsnorm_ms(T, H, threads, 1) for _ in range(args.steps)]
     wall = time.perf_counter() - t0
     us = 1e3 * sum(ms) / len(ms)
     line = {
-        "impl": "reference", "metric": METRIC, "value": us, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
+        "impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(us / 1e3, 3), "higher_is_better": False,
         "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic U(-1,1) inputs, unit weight",
-        "config": {"workload": f"reference rmsnorm_residual (TP=1 degenerate fused op), {T} tok x {H} hid",
+        "config": {"workload": f"TP=1 fused residual-add+RMSNorm, {T} tok x {H} hid (reference CPU path)",
                    "tokens": T, "hidden": H, "tp": 1},
-        "cpu_baseline": {"value": us, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"full workload per step ({T}x{H} fp32), token rows chunked over {threads} "
-                                   f"threads each calling weavesim::rmsnorm_residual; wall {wall:.1f}s"},
-        "e2e": {"value": us, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"full workload every step ({T}x{H} fp32): token rows chunked over {threads} "
+                                   f"threads, each calling weavesim::rmsnorm_residual; wall {wall:.1f}s"},
+        "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def k2_single_gpu(args):
+# ---- our arm, N = 1 -------------------------------------------------------------------
+
+def k2_timed(T, H, steps, warmup, flush, seed=0):
+    """Per-step CUDA-event times (ms) of K2 on a dedicated stream."""
     import torch
     import paper_2505_11329_b200 as tw
-
-    T, H = args.tokens, args.hidden
     dev = torch.device("cuda:0")
-    torch.cuda.set_device(dev)
-    stream = torch.cuda.Stream()
-    g = torch.Generator(device=dev).manual_seed(0)
+    g = torch.Generator(device=dev).manual_seed(seed)
     x = (torch.rand(T, H, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
     r = (torch.rand(T, H, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
     w = torch.rand(H, device=dev, generator=g) + 0.5
-    out = torch.empty_like(x)
-    rout = torch.empty_like(x)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # 256 MiB > 126 MB L2
-
-    def step():
-        tw.rmsnorm_residual(x, r, w, EPS, residual_out=rout, out=out, stream=stream)
-
+    out, rout = torch.empty_like(x), torch.empty_like(x)
+    stream = torch.cuda.Stream()
     with torch.cuda.stream(stream):
-        for _ in range(max(args.warmup, 3)):
-            step()
+        for _ in range(max(warmup, 3)):
+            tw.rmsnorm_residual(x, r, w, EPS, residual_out=rout, out=out, stream=stream)
     torch.cuda.synchronize()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    torch.cuda.synchronize()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
     with torch.cuda.stream(stream):
-        for i in range(args.steps):
-            flush.fill_(i & 0xFF)  # L2 flush, outside the event pair
+        for i in range(steps):
+            flush(i)
             starts[i].record(stream)
-            step()
+            tw.rmsnorm_residual(x, r, w, EPS, residual_out=rout, out=out, stream=stream)
             ends[i].record(stream)
     torch.cuda.synchronize()
-    times_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    return times_ms, (x, r, w, out, rout)
+    return [s.elapsed_time(e) for s, e in zip(starts, ends)], (x, r, w, out, rout)
 
 
-def k2_sweep(tokens_list, H, reps=20):
-    """Per-T K2 latency (same method) for the TP=1 column of the report."""
+def k2_e2e(T, H, bufs, steps):
+    """The same op through the public C-ABI with HOST buffers."""
     import torch
     import paper_2505_11329_b200 as tw
-    dev = torch.device("cuda:0")
-    res = {}
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    for T in tokens_list:
-        x = torch.randn(T, H, device=dev, dtype=torch.bfloat16)
-        r = torch.randn(T, H, device=dev, dtype=torch.bfloat16)
-        w = torch.ones(H, device=dev)
-        out, rout = torch.empty_like(x), torch.empty_like(x)
-        for _ in range(3):
-            tw.rmsnorm_residual(x, r, w, EPS, residual_out=rout, out=out)
-        ts = []
-        for i in range(reps):
-            flush.fill_(i & 0xFF)
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            tw.rmsnorm_residual(x, r, w, EPS, residual_out=rout, out=out)
-            e.record()
-            torch.cuda.synchronize()
-            ts.append(s.elapsed_time(e))
-        us = 1e3 * statistics.median(ts)
-        nbytes = 4 * T * H * 2 + 4 * H
-        res[str(T)] = {"us": round(us, 2), "hbm_gbs": round(nbytes / us / 1e3, 1)}
-    return res
-
-
-def unfused_baseline(T, H, reps=20):
-    """Unfused TP=1 baseline on the same box: torch add + torch rms_norm
-    (two kernels, the 'AR+RMSNorm' row's RMSNorm half without the AR)."""
-    import torch
-    dev = torch.device("cuda:0")
-    x = torch.randn(T, H, device=dev, dtype=torch.bfloat16)
-    r = torch.randn(T, H, device=dev, dtype=torch.bfloat16)
-    w = torch.ones(H, device=dev, dtype=torch.bfloat16)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    for _ in range(3):
-        y = torch.nn.functional.rms_norm(x + r, (H,), w, EPS)
-    ts = []
-    for i in range(reps):
-        flush.fill_(i & 0xFF)
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        rr = x + r
-        y = torch.nn.functional.rms_norm(rr, (H,), w, EPS)
-        e.record()
-        torch.cuda.synchronize()
-        ts.append(s.elapsed_time(e))
-    return round(1e3 * statistics.median(ts), 2)
-
-
-def k2_e2e(args, bufs):
-    """Same op through the public C-ABI with HOST buffers: pinned H2D of input
-    and residual, the kernel, D2H of output and residual_out, per step."""
-    import torch
-    import paper_2505_11329_b200 as tw
-    T, H = args.tokens, args.hidden
     x, r, w, out, rout = bufs
     hx = torch.empty(T, H, dtype=torch.bfloat16, pin_memory=True)
     hr = torch.empty(T, H, dtype=torch.bfloat16, pin_memory=True)
@@ -246,7 +197,6 @@ def k2_e2e(args, bufs):
     hx.copy_(x)
     hr.copy_(r)
     stream = torch.cuda.Stream()
-    steps = max(3, min(args.steps, 20))
 
     def step():
         x.copy_(hx, non_blocking=True)
@@ -265,63 +215,113 @@ def k2_e2e(args, bufs):
             step()
         e.record(stream)
     torch.cuda.synchronize()
-    us = 1e3 * s.elapsed_time(e) / steps
     nb = T * H * 2
-    return {"value": round(us, 2), "unit": UNIT, "h2d_bytes_per_step": 2 * nb, "d2h_bytes_per_step": 2 * nb,
-            "steps": steps, "path": "tw_rmsnorm_residual via ctypes C-ABI, pinned host buffers"}
+    return {"value": round(1e3 * s.elapsed_time(e) / steps, 2), "unit": UNIT, "h2d_bytes_per_step": 2 * nb,
+            "d2h_bytes_per_step": 2 * nb, "steps": steps,
+            "path": "tw_rmsnorm_residual (C-ABI via ctypes), pinned host input/residual -> device -> host"}
 
 
-def load_profile_traffic(name):
-    p = os.path.join(ROOT, "profiles", name)
-    try:
-        with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
-    except Exception:
-        return None
+def unfused_torch(T, H, flush, reps=20):
+    """Unfused TP=1 baseline on the same box: torch add + torch rms_norm."""
+    import torch
+    x = torch.randn(T, H, device="cuda", dtype=torch.bfloat16)
+    r = torch.randn(T, H, device="cuda", dtype=torch.bfloat16)
+    w = torch.ones(H, device="cuda", dtype=torch.bfloat16)
+    for _ in range(3):
+        torch.nn.functional.rms_norm(x + r, (H,), w, EPS)
+    ts = []
+    for i in range(reps):
+        flush(i)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch.nn.functional.rms_norm(x + r, (H,), w, EPS)
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    return round(1e3 * statistics.median(ts), 2)
+
+
+def k1_colocated(T, H, world, budget, flush, reps=10):
+    """K1 with `world` simulated ranks on this GPU (PEER transport): a
+    correctness-scale check of the fused path at full size.  HBM-bound here,
+    NOT an NVLink number."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    comm = tw.Communicator(world, [0] * world, T * H * 2, tw.TW_TRANSPORT_PEER)
+    for q in range(world):
+        comm.buffer(q, tw.TW_BUF_INPUT, (T, H), torch.bfloat16).normal_()
+    ranges = tw.token_shard_map(T, world)
+    shards = [torch.randn(e - b, H, device="cuda", dtype=torch.bfloat16) for b, e in ranges]
+    w = [torch.ones(H, device="cuda")] * world
+    for _ in range(3):
+        comm.fused_allreduce_rmsnorm(T, H, shards, w, sm_budget=budget)
+    ts = []
+    for i in range(reps):
+        flush(i)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        comm.fused_allreduce_rmsnorm(T, H, shards, w, sm_budget=budget)
+        e.record()
+        torch.cuda.synchronize()
+        ts.append(s.elapsed_time(e))
+    comm.check()
+    comm.close()
+    return round(1e3 * statistics.median(ts), 1)
 
 
 def run_ours_single(args):
     import torch
     T, H = args.tokens, args.hidden
-    peak, peak_kind = measured_peaks()
+    torch.cuda.set_device(0)
+    flush = L2Flush("cuda:0")
+    peak, peak_kind = measured_hbm_peak()
     with ClockSampler(0) as clk:
         t0 = time.perf_counter()
-        times_ms, bufs = k2_single_gpu(args)
-        e2e = k2_e2e(args, bufs)
+        times_ms, bufs = k2_timed(T, H, args.steps, args.warmup, flush)
+        e2e = k2_e2e(T, H, bufs, max(3, min(args.steps, 20)))
         wall = time.perf_counter() - t0
     avg_us = 1e3 * sum(times_ms) / len(times_ms)
-    alg_bytes = 4 * T * H * 2 + 4 * H  # read in+res, write res_out+out (bf16), read fp32 weight
+    alg_bytes = 4 * T * H * 2 + 4 * H  # read input+residual, write residual_out+output (bf16) + fp32 weight
     achieved = alg_bytes / (avg_us * 1e-6) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "k2_ncu_r01.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
     line = {
         "metric": METRIC, "value": round(avg_us, 3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(avg_us / 1e3, 6), "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic U(-1,1) bf16 activations, U(0.5,1.5) fp32 weight",
-        "config": {"workload": f"TP=1 fused residual-add+RMSNorm (K2), {T} tok x {H} hid bf16 "
-                               "(Qwen2.5-72B/Llama-3.3-70B layer-boundary shape)",
-                   "tokens": T, "hidden": H, "tp": 1, "l2": "flushed between steps (256 MiB write)",
-                   "sm_budget": "whole GPU"},
+        "data": "synthetic: U(-1,1) bf16 input/residual, U(0.5,1.5) fp32 weight",
+        "config": {"workload": f"TP=1 fused residual-add+RMSNorm (kernel K2), {T} tok x {H} hid bf16 "
+                               "(Qwen2.5-72B / Llama-3.3-70B layer-boundary shape, BASELINE configs[2] at TP=1)",
+                   "tokens": T, "hidden": H, "tp": 1, "sm_budget": "whole GPU (148 SMs)", "l2": FLUSH_NOTE},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
-                     "alg_bytes_per_launch": alg_bytes,
-                     "traffic": load_profile_traffic("k2_ncu_r01.json")},
+                     "alg_bytes_per_launch": alg_bytes, "traffic": traffic},
         "e2e": e2e,
         "gpu_launches": args.steps,
-        "kernel_us": {"median": round(1e3 * statistics.median(times_ms), 3), "min": round(1e3 * min(times_ms), 3),
-                      "max": round(1e3 * max(times_ms), 3)},
+        "kernel_us": {"median": round(1e3 * statistics.median(times_ms), 3),
+                      "min": round(1e3 * min(times_ms), 3), "max": round(1e3 * max(times_ms), 3)},
+        "clocks": clk.summary(),
     }
-    clocks = clk.summary()
-    line["clocks"] = clocks
     if not args.quick:
-        line["tp1_sweep"] = k2_sweep([1024, 2048, 4096, 8192], H)
-        line["unfused_torch_add_rmsnorm_us"] = unfused_baseline(T, H)
+        sweep = {}
+        for t in (1024, 2048, 4096, 8192):
+            ts, _ = k2_timed(t, H, 20, 3, flush, seed=1)
+            us = 1e3 * statistics.median(ts)
+            sweep[str(t)] = {"us": round(us, 2), "hbm_gbs": round((4 * t * H * 2) / us / 1e3, 1)}
+        line["tp1_sweep"] = sweep
+        line["unfused_torch_add_rmsnorm_us"] = unfused_torch(T, H, flush)
+        line["k1_colocated_peer_us"] = {f"tp{n}": k1_colocated(T, H, n, 16, flush) for n in (2, 8)}
         threads = os.cpu_count() or 1
         sample_T = 2048
-        ms = cpu_reference_times(sample_T, H, 3, threads)
-        cpu_us = 1e3 * statistics.median(ms) * (T / sample_T)
-        line["cpu_baseline"] = {"value": round(cpu_us, 1), "unit": UNIT, "cores": threads, "kind": "reference",
-                                "sample": f"weavesim::rmsnorm_residual (oracle/_ref) on {sample_T}x{H} fp32, "
-                                          f"median of 3, scaled x{T // sample_T} to {T} tokens"}
+        cpu_ms = reference_rmsnorm_ms(sample_T, H, threads, 3)
+        line["cpu_baseline"] = {
+            "value": round(1e3 * cpu_ms * T / sample_T, 1), "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"weavesim::rmsnorm_residual (oracle/_ref, reference sources compiled unmodified) on "
+                      f"{sample_T}x{H} fp32 rows over {threads} threads, median of 3, scaled x{T // sample_T}"}
     line["wall_s"] = round(wall, 2)
     print(json.dumps(line), flush=True)
     return 0
@@ -333,15 +333,16 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--tokens", type=int, default=T_DEFAULT)
-    ap.add_argument("--hidden", type=int, default=H_DEFAULT)
+    ap.add_argument("--tokens", type=int, default=8192)
+    ap.add_argument("--hidden", type=int, default=8192)
+    ap.add_argument("--sm-budget", type=int, default=16, help="K1 CTAs per rank (N>1)")
+    ap.add_argument("--gather-residual", action="store_true", help="K1 G=2 (N>1)")
     ap.add_argument("--quick", action="store_true", help="skip sweeps/baselines (profiling runs)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
-        from tools.bench_tp import run_tp  # multi-process TP=N path
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        from tools.bench_tp import run_tp
         return run_tp(args)
     return run_ours_single(args)
 

@@ -137,6 +137,25 @@ TW_API tw_status tw_fused_allreduce_rmsnorm_group(tw_comm_t comm, int64_t T, int
                                            void* const* residual_shards, const float* const* weights, float eps,
                                            tw_dtype dtype, int sm_budget, unsigned flags, void* const* streams);
 
+/* --- Multi-process communicators (one process per GPU, e.g. torchrun) ---------
+ * Every rank calls tw_comm_create_mp with the same world, buffer_bytes and
+ * rendezvous_id (a job-unique string, e.g. broadcast by the launcher); rank 0
+ * creates the NVLS multicast object and shares it by POSIX fd over an
+ * abstract Unix socket.  Collective per-rank calls must be made in the same
+ * order with the same shapes on every rank (the signal-pad epochs are
+ * host-tracked).  Transport is always NVLS. */
+TW_API tw_status tw_comm_create_mp(int world, int rank, int device, size_t buffer_bytes, const char* rendezvous_id,
+                                   tw_comm_t* out);
+/* K1 for the rank this process owns (multi-process communicators). */
+TW_API tw_status tw_fused_allreduce_rmsnorm(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset,
+                                            const int64_t* shard_ranges, void* residual_shard, const float* weight,
+                                            float eps, tw_dtype dtype, int sm_budget, unsigned flags, void* stream);
+TW_API tw_status tw_allreduce(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset, tw_dtype dtype,
+                              int sm_budget, void* stream);
+/* The rendezvous used by tw_comm_create_mp, exposed for host-side tests: rank
+ * 0's `fd` is delivered to every rank as *fd_out (then a barrier). */
+TW_API tw_status tw_rendezvous_exchange_fd(const char* rendezvous_id, int world, int rank, int fd, int* fd_out);
+
 /* --- Unfused baselines (NOT the product path) ---------------------------------
  * all_reduce (collectives.cpp:82-88) over the communicator: OUTPUT[t] = sum_r INPUT[t]
  * for every t (one-shot NVLS ld_reduce + multimem.st, or PEER loads). */

@@ -71,12 +71,14 @@ const Driver& driver() {
     resolve(d.memUnmap, "cuMemUnmap", ok);
     resolve(d.memSetAccess, "cuMemSetAccess", ok);
     resolve(d.getErrorString, "cuGetErrorString", ok);
+    resolve(d.exportHandle, "cuMemExportToShareableHandle", ok);
+    resolve(d.importHandle, "cuMemImportFromShareableHandle", ok);
     d.ok = ok;
   });
   return d;
 }
 
-static std::string cu_str(CUresult r) {
+std::string cu_str(CUresult r) {
   const char* s = nullptr;
   if (driver().getErrorString) driver().getErrorString(r, &s);
   return s ? s : ("CUresult " + std::to_string(static_cast<int>(r)));
@@ -93,7 +95,7 @@ static int sm_count(int device) {
   return cache[device];
 }
 
-static size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 struct DeviceGuard {
@@ -217,9 +219,10 @@ static tw_status create_nvls(tw_comm* c) {
   return TW_OK;
 }
 
-static void destroy_comm(tw_comm* c) {
+void destroy_comm(tw_comm* c) {
   const Driver& d = driver();
   for (RankBuffers& rb : c->ranks) {
+    if (!rb.buf[0] && !rb.phys && !rb.uc_base && !rb.mc_base) continue;  // not owned by this process
     cudaSetDevice(rb.device);
     cudaDeviceSynchronize();
     if (rb.owns_cuda_malloc && rb.buf[0]) cudaFree(rb.buf[0]);
@@ -312,13 +315,54 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
   const int nv = bf16 ? 8 : 4;
   const bool vec = H % nv == 0 && aligned16(input) && aligned16(residual) && aligned16(residual_out) &&
                    aligned16(output) && aligned16(weight);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int nsm = sm_count(dev);
+  const int sms = sm_budget > 0 ? std::min(sm_budget, nsm) : nsm;
+  // Preferred engine: the warp-specialised bulk-copy pipeline (16-B aligned
+  // rows, H % (16/elem) == 0).  TW_K2_ENGINE=rows forces the row engine.
+  static const char* engine_env = std::getenv("TW_K2_ENGINE");
+  // Default by row size (measured on B200, profiles/k2_engines_r01.txt): rows
+  // >= 16 KB -> TMA loads + TMA stores; 12-16 KB -> TMA loads + register
+  // stores; smaller rows -> the register row engine (per-row barrier and bulk
+  // issue costs dominate short rows).
+  const size_t rbytes = static_cast<size_t>(H) * (bf16 ? 2 : 4);
+  bool want_rows = rbytes < 12 * 1024;
+  bool tma_store = rbytes >= 16 * 1024;
+  if (engine_env) {
+    want_rows = std::strcmp(engine_env, "rows") == 0;
+    tma_store = std::strcmp(engine_env, "tma") == 0;
+  }
+  if (vec && !want_rows) {
+    RowPlan bp;
+    const uint32_t row_bytes = static_cast<uint32_t>(H * (bf16 ? 2 : 4));
+    const size_t smem_budget = 200 * 1024;
+    const int stages = static_cast<int>(std::min<size_t>(8, smem_budget / (2ull * row_bytes)));
+    if (plan_rows(H, nv, H / nv > 1024 ? 512 : 256, &bp) && bp.vpt <= 8 && bp.tpr <= kBulkMaxConsumers &&
+        stages >= 2) {
+      BulkParams q = {};
+      q.in = input;
+      q.res_in = residual;
+      q.res_out = residual_out;
+      q.out = output;
+      q.weight = weight;
+      q.T = T;
+      q.H = H;
+      q.V = bp.V;
+      q.tpr = bp.tpr;
+      q.stages = stages;
+      q.row_bytes = row_bytes;
+      q.eps = eps;
+      const int grid = static_cast<int>(std::min<long long>(T, sms));
+      cudaError_t e = launch_k2_bulk(q, bp.vpt, bf16, grid, static_cast<cudaStream_t>(stream), tma_store);
+      if (e != cudaSuccess) return cuda_fail(e, "rmsnorm_residual (bulk) launch");
+      return TW_OK;
+    }
+  }
   RowPlan plan;
   if (!plan_rows(H, vec ? nv : 1, 256, &plan))
     return fail(TW_ERR_DIMENSION, "rmsnorm_residual: hidden size too large for the row engine");
-  int dev = 0;
-  cudaGetDevice(&dev);
   const int bpsm = std::max(1, rownorm_blocks_per_sm(plan, bf16, Xport::Local));
-  const int sms = sm_budget > 0 ? std::min(sm_budget, sm_count(dev)) : sm_count(dev);
   const long long need = (T + plan.groups - 1) / plan.groups;
   const int grid = static_cast<int>(std::min<long long>(need, static_cast<long long>(sms) * bpsm));
   RowParams p = {};
@@ -506,9 +550,11 @@ tw_status tw_comm_check(tw_comm_t comm) {
 
 }  // extern "C"
 
-namespace {
+namespace tw {
 
 // Common validation + launch for the fused op (K1) and the AR baseline (K3).
+// Single-process communicators launch every rank; a multi-process
+// communicator (local_rank >= 0) launches only the rank this process owns.
 tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset, const int64_t* shard_ranges, void* const* residual_shards,
                       const float* const* weights, float eps, tw_dtype dtype, int sm_budget, unsigned flags,
                       void* const* streams, bool fused) {
@@ -530,11 +576,13 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
   }
   tw_status st = tw_shard_map_validate(shard_ranges, W, T);
   if (st != TW_OK) return st;
+  auto owned = [&](int r) { return comm->local_rank < 0 || r == comm->local_rank; };
   if (fused) {
     if (!(eps > 0.0f) && eps != 0.0f) return fail(TW_ERR_NUMERIC, "fused_allreduce_rmsnorm: epsilon must be nonnegative");
     if (!weights) return fail(TW_ERR_DIMENSION, "fused_allreduce_rmsnorm: null weight list");
     if (!residual_shards) return fail(TW_ERR_DIMENSION, "fused_allreduce_rmsnorm: null residual list");
     for (int r = 0; r < W; ++r) {
+      if (!owned(r)) continue;
       if (!weights[r]) return fail(TW_ERR_DIMENSION, "fused_allreduce_rmsnorm: null weight");
       if (shard_ranges[2 * r + 1] > shard_ranges[2 * r] && !residual_shards[r])
         return fail(TW_ERR_DIMENSION, "fused_allreduce_rmsnorm: null residual shard");
@@ -546,6 +594,7 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
   bool vec = H % nv == 0;
   if (fused) {
     for (int r = 0; r < W && vec; ++r) {
+      if (!owned(r)) continue;
       vec = aligned16(weights[r]) && (residual_shards[r] == nullptr || aligned16(residual_shards[r]));
     }
   }
@@ -559,7 +608,7 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
 
   DeviceGuard guard;
   int budget = sm_budget > 0 ? sm_budget : 8;
-  const int dev0 = comm->ranks[0].device;
+  const int dev0 = comm->ranks[comm->local_rank < 0 ? 0 : comm->local_rank].device;
   cudaSetDevice(dev0);
   const int sms = sm_count(dev0);
   if (fused) {
@@ -606,6 +655,7 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
     if (e != cudaSuccess) return cuda_fail(e, op);
   } else {
     for (int r = 0; r < W; ++r) {
+      if (!owned(r)) continue;
       cudaSetDevice(comm->ranks[r].device);
       RowParams pr = p;
       pr.nslots = 1;
@@ -626,7 +676,7 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
   return TW_OK;
 }
 
-}  // namespace
+}  // namespace tw
 
 extern "C" {
 

@@ -39,6 +39,9 @@ struct Driver {
   CUresult (*memUnmap)(CUdeviceptr, size_t) = nullptr;
   CUresult (*memSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
   CUresult (*getErrorString)(CUresult, const char**) = nullptr;
+  CUresult (*exportHandle)(void*, CUmemGenericAllocationHandle, CUmemAllocationHandleType, unsigned long long) =
+      nullptr;
+  CUresult (*importHandle)(CUmemGenericAllocationHandle*, void*, CUmemAllocationHandleType) = nullptr;
 };
 const Driver& driver();
 
@@ -67,4 +70,14 @@ struct tw_comm {
   std::vector<tw::RankBuffers> ranks;
   CUmemGenericAllocationHandle mc = 0;
   uint64_t arrivals = 0;    // cumulative signal-pad arrivals per rank (host mirror)
+  int local_rank = -1;      // >= 0: multi-process communicator owning only this rank
 };
+
+namespace tw {
+tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset, const int64_t* shard_ranges,
+                      void* const* residual_shards, const float* const* weights, float eps, tw_dtype dtype,
+                      int sm_budget, unsigned flags, void* const* streams, bool fused);
+size_t round_up(size_t x, size_t a);
+std::string cu_str(CUresult r);
+void destroy_comm(tw_comm* c);
+}  // namespace tw

@@ -193,3 +193,148 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_bulk_kernel(cons
 }
 
 }  // namespace tw
+
+namespace tw {
+
+// Shared -> global bulk copy (TMA bulk engine), tracked by bulk async-groups.
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void sts_v4(void* p, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(smem_addr(p)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+// K2 v2: TMA bulk engine on BOTH sides.  Loads as in k2_bulk_kernel; the
+// consumers write r' over the residual slot and the output over the input
+// slot of the same stage, and one consumer thread (the "storer") issues two
+// shared->global bulk stores per row.  A stage returns to the producer only
+// after the bulk engine has finished READING it (bulk_wait_read<1> lags one
+// row so the store of row i overlaps the math of row i+1).  The SM's load/
+// store units only touch shared memory; HBM traffic is issued by TMA.
+template <class E, int VPT>
+__global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const __grid_constant__ BulkParams p) {
+  constexpr int N = 16 / sizeof(E);
+  using VT = Vec<E, N>;
+  using Acc = typename std::conditional<sizeof(E) == 4, double, float>::type;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int S = p.stages;
+  unsigned char* ring = smem;  // [S][2][row_bytes]: slot 0 input/output, slot 1 residual/r'
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(S) * 2 * p.row_bytes);
+  uint64_t* empty = full + S;
+  Acc* part = reinterpret_cast<Acc*>(empty + S);
+
+  const int tpr = p.tpr;
+  const int cwarps = tpr >> 5;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);  // released by the storer only
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const long long nrows = p.T > blockIdx.x ? (p.T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (long long i = 0; i < nrows; ++i) {
+        const int s = static_cast<int>(i % S);
+        const uint32_t ph = static_cast<uint32_t>((i / S) & 1);
+        if (i >= S) mbar_wait(&empty[s], ph ^ 1u);
+        const long long row = blockIdx.x + i * gridDim.x;
+        unsigned char* dst = ring + static_cast<size_t>(s) * 2 * p.row_bytes;
+        mbar_arrive_expect_tx(&full[s], 2 * p.row_bytes);
+        bulk_g2s(dst, static_cast<const unsigned char*>(p.in) + row * p.row_bytes, p.row_bytes, &full[s]);
+        bulk_g2s(dst + p.row_bytes, static_cast<const unsigned char*>(p.res_in) + row * p.row_bytes, p.row_bytes,
+                 &full[s]);
+      }
+    }
+    return;
+  }
+
+  const int lt = threadIdx.x - 32;
+  const int cw = warp - 1;
+  const bool storer = lt == 0;
+  float w[VPT][N];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int c = lt + k * tpr;
+    if (c < p.V) load_weight<N>(p.weight, static_cast<long long>(c) * N, w[k]);
+  }
+  for (long long i = 0; i < nrows; ++i) {
+    const int s = static_cast<int>(i % S);
+    const uint32_t ph = static_cast<uint32_t>((i / S) & 1);
+    const long long row = blockIdx.x + i * gridDim.x;
+    unsigned char* st = ring + static_cast<size_t>(s) * 2 * p.row_bytes;
+    mbar_wait(&full[s], ph);
+    typename VT::Raw rr[VPT];
+    Acc ss = 0;
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int c = lt + k * tpr;
+      if (c < p.V) {
+        float x[N], r[N];
+        VT::unpack(lds_v4(st + c * 16), x);
+        VT::unpack(lds_v4(st + p.row_bytes + c * 16), r);
+#pragma unroll
+        for (int j = 0; j < N; ++j) r[j] = x[j] + r[j];
+        rr[k] = VT::pack(r);
+        VT::unpack(rr[k], r);
+#pragma unroll
+        for (int j = 0; j < N; ++j) ss += static_cast<Acc>(r[j]) * static_cast<Acc>(r[j]);
+        sts_v4(st + p.row_bytes + c * 16, rr[k]);  // r' over the residual slot
+      }
+    }
+    ss = warp_sum(ss);
+    Acc total;
+    Acc* pp = part + (i & 1) * cwarps;
+    if (lane == 0) pp[cw] = ss;
+    named_bar_sync(1, tpr);
+    total = 0;
+    for (int q = 0; q < cwarps; ++q) total += pp[q];
+    const float inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(p.H)) + p.eps);
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int c = lt + k * tpr;
+      if (c < p.V) {
+        float o[N];
+        VT::unpack(rr[k], o);
+#pragma unroll
+        for (int j = 0; j < N; ++j) o[j] = o[j] * inv * w[k][j];
+        sts_v4(st + c * 16, VT::pack(o));  // output over the input slot
+      }
+    }
+    fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk engine
+    named_bar_sync(1, tpr);
+    if (storer) {
+      bulk_s2g(static_cast<unsigned char*>(p.out) + row * p.row_bytes, st, p.row_bytes);
+      bulk_s2g(static_cast<unsigned char*>(p.res_out) + row * p.row_bytes, st + p.row_bytes, p.row_bytes);
+      bulk_commit();
+      // the previous row's stores have finished reading their stage: free it
+      if (i > 0) {
+        bulk_wait_read<1>();
+        mbar_arrive(&empty[(i - 1) % S]);
+      }
+    }
+  }
+  if (storer) {
+    bulk_wait_all();
+    if (nrows > 0) mbar_arrive(&empty[(nrows - 1) % S]);
+  }
+}
+
+}  // namespace tw

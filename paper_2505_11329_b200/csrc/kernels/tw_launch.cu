@@ -145,12 +145,12 @@ namespace {
 using BulkFn = void (*)(BulkParams);
 
 template <class E>
-BulkFn pick_bulk_e(int vpt) {
+BulkFn pick_bulk_e(int vpt, bool tma_store) {
   switch (vpt) {
-    case 1: return k2_bulk_kernel<E, 1>;
-    case 2: return k2_bulk_kernel<E, 2>;
-    case 4: return k2_bulk_kernel<E, 4>;
-    case 8: return k2_bulk_kernel<E, 8>;
+    case 1: return tma_store ? k2_tma_kernel<E, 1> : k2_bulk_kernel<E, 1>;
+    case 2: return tma_store ? k2_tma_kernel<E, 2> : k2_bulk_kernel<E, 2>;
+    case 4: return tma_store ? k2_tma_kernel<E, 4> : k2_bulk_kernel<E, 4>;
+    case 8: return tma_store ? k2_tma_kernel<E, 8> : k2_bulk_kernel<E, 8>;
     default: return nullptr;
   }
 }
@@ -160,8 +160,9 @@ size_t bulk_smem_bytes(int stages, uint32_t row_bytes, int tpr) {
   return static_cast<size_t>(stages) * 2 * row_bytes + 2 * stages * sizeof(uint64_t) + 2 * (tpr / 32) * sizeof(double);
 }
 
-cudaError_t launch_k2_bulk(const BulkParams& params, int vpt, bool bf16, int grid, cudaStream_t stream) {
-  BulkFn fn = bf16 ? pick_bulk_e<uint16_t>(vpt) : pick_bulk_e<float>(vpt);
+cudaError_t launch_k2_bulk(const BulkParams& params, int vpt, bool bf16, int grid, cudaStream_t stream,
+                           bool tma_store) {
+  BulkFn fn = bf16 ? pick_bulk_e<uint16_t>(vpt, tma_store) : pick_bulk_e<float>(vpt, tma_store);
   if (!fn) return cudaErrorInvalidConfiguration;
   const size_t smem = bulk_smem_bytes(params.stages, params.row_bytes, params.tpr);
   cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,

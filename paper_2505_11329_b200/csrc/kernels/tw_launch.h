@@ -27,7 +27,8 @@ cudaError_t launch_allreduce(const RowParams& params, const RowPlan& plan, bool 
                              cudaStream_t stream);
 int rownorm_blocks_per_sm(const RowPlan& plan, bool bf16, Xport x);
 size_t bulk_smem_bytes(int stages, uint32_t row_bytes, int tpr);
-cudaError_t launch_k2_bulk(const BulkParams& params, int vpt, bool bf16, int grid, cudaStream_t stream);
+cudaError_t launch_k2_bulk(const BulkParams& params, int vpt, bool bf16, int grid, cudaStream_t stream,
+                           bool tma_store);
 cudaError_t launch_count_nonfinite(const void* x, long long n, bool bf16, int* count, cudaStream_t stream);
 
 }  // namespace tw

@@ -1,0 +1,67 @@
+"""Multi-process host logic on CPU (gloo, world_size 2): the rendezvous that
+shares the NVLS multicast handle by file descriptor, the job-unique id
+broadcast and the max-over-ranks timing reduction used by bench.py's TP leg."""
+import os
+import socket
+import subprocess
+import sys
+import textwrap
+
+from tests.conftest import ROOT
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+WORKER = textwrap.dedent("""
+    import ctypes, os, sys
+    sys.path.insert(0, {root!r})
+    import torch.distributed as dist
+    from tools.bench_tp import rendezvous_id, max_over_ranks
+    from paper_2505_11329_b200 import _lib
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    rid = rendezvous_id(dist)
+    fd = -1
+    if rank == 0:
+        fd = os.memfd_create("tw-test")
+        os.write(fd, b"multicast-handle-stand-in")
+    out = ctypes.c_int(-1)
+    _lib.check(_lib.lib.tw_rendezvous_exchange_fd(rid.encode(), world, rank, fd, ctypes.byref(out)))
+    os.lseek(out.value, 0, os.SEEK_SET)
+    got = os.read(out.value, 64)
+    assert got == b"multicast-handle-stand-in", got
+    m = max_over_ranks(10.0 + rank, dist)
+    assert m == 10.0 + world - 1, m
+    ids = [None] * world
+    dist.all_gather_object(ids, rid)
+    assert len(set(ids)) == 1
+    print("rank", rank, "ok", flush=True)
+    dist.destroy_process_group()
+""")
+
+
+def test_rendezvous_and_reductions_gloo_world2(tmp_path):
+    script = tmp_path / "worker.py"
+    script.write_text(WORKER.format(root=ROOT))
+    port = free_port()
+    procs = []
+    for rank in range(2):
+        env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE="2")
+        procs.append(subprocess.Popen([sys.executable, str(script)], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.STDOUT, text=True))
+    outs = [p.communicate(timeout=180)[0] for p in procs]
+    for rank, (p, o) in enumerate(zip(procs, outs)):
+        assert p.returncode == 0, o
+        assert f"rank {rank} ok" in o
+
+
+def test_nvlink_roofline_bytes():
+    from tools.bench_tp import algorithmic_nvlink_bytes
+    # SURVEY.md §8d worked numbers: N=8, G=1, T=1024 -> 18.87 MB; T=8192 -> 150.99 MB; G=2 T=8192 -> 285.2 MB
+    assert abs(algorithmic_nvlink_bytes(1024, 8192, 8, False) / 1e6 - 18.87) < 0.01
+    assert abs(algorithmic_nvlink_bytes(8192, 8192, 8, False) / 1e6 - 150.99) < 0.01
+    assert abs(algorithmic_nvlink_bytes(8192, 8192, 8, True) / 1e6 - 285.21) < 0.01

@@ -34,11 +34,15 @@ def run(H=8192, tokens=(1024, 2048, 4096, 8192, 16384), reps=30):
     return out
 
 
+def H_label():
+    return os.environ.get("TW_K2_ENGINE", "tma") + " H=" + sys.argv[2]
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "child":
-        print(os.environ.get("TW_K2_ENGINE", "bulk"), run(H=int(sys.argv[2])))
+        print(H_label(), run(H=int(sys.argv[2])))
     else:
         for H in (8192, 4096, 6144):
-            for eng in ("bulk", "rows"):
+            for eng in ("tma", "bulk", "rows"):
                 env = dict(os.environ, TW_K2_ENGINE=eng)
                 subprocess.run([sys.executable, __file__, "child", str(H)], env=env, check=True)
