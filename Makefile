@@ -38,7 +38,11 @@ $(OBJDIR)/tw_mp.o: $(MPSRC) $(HHDR) $(KHDR)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(LIBDIR)/libtw.so: $(OBJDIR)/tw_launch.o $(OBJDIR)/tw_capi.o $(OBJDIR)/tw_mp.o
+$(OBJDIR)/tw_host_io.o: $(PKG)/csrc/host/tw_host_io.cu $(HHDR) $(KHDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIBDIR)/libtw.so: $(OBJDIR)/tw_launch.o $(OBJDIR)/tw_capi.o $(OBJDIR)/tw_mp.o $(OBJDIR)/tw_host_io.o
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -Xlinker --exclude-libs,ALL
 

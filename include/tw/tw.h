@@ -67,7 +67,6 @@ typedef enum tw_buffer {
 
 /* Flags for the fused op. */
 #define TW_GATHER_RESIDUAL 0x1u /* G=2: all-gather r' as well as the output  */
-#define TW_CHECK_FINITE 0x2u    /* device-side NaN/Inf scan -> TW_ERR_NUMERIC */
 
 typedef struct tw_comm* tw_comm_t;
 
@@ -90,6 +89,14 @@ TW_API int tw_device_count(void);
 TW_API tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* residual_out, void* output,
                               const float* weight, int64_t T, int64_t H, float eps, tw_dtype dtype,
                               int sm_budget, void* stream);
+
+/* K2 over HOST buffers (pinned for full speed): chunks of chunk_rows rows
+ * (<= 0: ~8 MiB) are pipelined over a ring of streams -- H2D of chunk k+1,
+ * the kernel on chunk k and D2H of chunk k-1 overlap.  Work is ordered after
+ * `stream`'s prior work and `stream` waits for completion (no host sync). */
+TW_API tw_status tw_rmsnorm_residual_host(const void* h_input, const void* h_residual, void* h_residual_out,
+                                          void* h_output, const float* h_weight, int64_t T, int64_t H, float eps,
+                                          tw_dtype dtype, int64_t chunk_rows, void* stream);
 
 /* Device-side finite scan: *nonfinite_count (device int32) += #NaN/Inf in x.
  * Replaces TokenMatrix::validate's isfinite loop (numerics.cpp:25-27). */

@@ -84,6 +84,30 @@ def rmsnorm_residual(inp, residual, weight, eps: float = 1e-5, *, residual_out=N
     return out, residual_out
 
 
+def rmsnorm_residual_host(inp, residual, weight, eps: float = 1e-5, *, residual_out=None, out=None,
+                          chunk_rows: int = 0, stream=None):
+    """K2 over HOST (CPU) tensors -- pin them for full speed.  The C-ABI
+    pipelines chunks (H2D | kernel | D2H overlapped); on return the work is
+    enqueued on `stream` (synchronize before reading the outputs)."""
+    import torch
+    if inp.dim() != 2 or residual.shape != inp.shape:
+        raise DimensionError("rmsnorm_residual_host: input and residual shapes differ")
+    T, H = inp.shape
+    if weight.numel() != H or weight.dtype != torch.float32 or weight.is_cuda:
+        raise DimensionError("rmsnorm_residual_host: weight must be a host fp32 [H] tensor")
+    if out is None:
+        out = torch.empty_like(inp)
+    if residual_out is None:
+        residual_out = torch.empty_like(inp)
+    for t in (inp, residual, residual_out, out):
+        if t.is_cuda or not t.is_contiguous():
+            raise ConfigError("rmsnorm_residual_host: tensors must be contiguous host tensors")
+    check(_lib.lib.tw_rmsnorm_residual_host(_ptr(inp), _ptr(residual), _ptr(residual_out), _ptr(out), _ptr(weight),
+                                            T, H, float(eps), _dtype_code(inp), int(chunk_rows),
+                                            _stream_handle(stream)))
+    return out, residual_out
+
+
 class _DevBuf:
     """__cuda_array_interface__ view of communicator memory (no ownership)."""
 

@@ -72,6 +72,8 @@ _SIGNATURES = [
     ("tw_device_count", c_int, []),
     ("tw_rmsnorm_residual", c_int,
      [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_int, c_int, c_void_p]),
+    ("tw_rmsnorm_residual_host", c_int,
+     [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_int, c_int64, c_void_p]),
     ("tw_count_nonfinite", c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p]),
     ("tw_token_shard_map", c_int, [c_int64, c_int, POINTER(c_int64)]),
     ("tw_shard_map_validate", c_int, [POINTER(c_int64), c_int, c_int64]),

@@ -602,7 +602,10 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
     return fail(TW_ERR_UNSUPPORTED, std::string(op) + ": NVLS transport needs H % " + std::to_string(nv) +
                                         " == 0 and 16-byte aligned buffers");
   RowPlan plan;
-  if (!plan_rows(H, vec ? nv : 1, nvls ? 128 : 256, &plan))
+  // NVLS: 128-thread row groups (4 rows in flight per CTA); PEER holds every
+  // rank's vector in registers before summing, so it uses wider groups
+  // (fewer vectors per thread) to stay spill-free.
+  if (!plan_rows(H, vec ? nv : 1, nvls ? 128 : 512, &plan))
     return fail(TW_ERR_DIMENSION, std::string(op) + ": hidden size too large for the row engine");
   const Xport x = nvls ? Xport::Nvls : Xport::Peer;
 

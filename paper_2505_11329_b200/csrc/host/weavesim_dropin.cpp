@@ -153,22 +153,13 @@ NormResult rmsnorm_residual(const TokenMatrix& input, const TokenMatrix& residua
   result.residual_out = TokenMatrix::zeros(T, H);
   if (T == 0) return result;
   device_count_or_throw();
-  const size_t nb = static_cast<size_t>(T * H) * sizeof(float);
   std::lock_guard<std::mutex> lock(g_mu);
-  static DevBuf d_in, d_res, d_out, d_rout, d_w;
-  d_in.reserve(0, nb);
-  d_res.reserve(0, nb);
-  d_out.reserve(0, nb);
-  d_rout.reserve(0, nb);
-  d_w.reserve(0, H * sizeof(float));
-  check(tw_memcpy(d_in.ptr, input.values.data(), nb, nullptr), "rmsnorm_residual: H2D");
-  check(tw_memcpy(d_res.ptr, residual.values.data(), nb, nullptr), "rmsnorm_residual: H2D");
-  check(tw_memcpy(d_w.ptr, params.weight.data(), H * sizeof(float), nullptr), "rmsnorm_residual: H2D");
-  check(tw_rmsnorm_residual(d_in.ptr, d_res.ptr, d_rout.ptr, d_out.ptr, static_cast<const float*>(d_w.ptr), T, H,
-                            params.epsilon, TW_F32, 0, nullptr),
+  // Host matrices in, host matrices out: the chunked H2D | K2 | D2H pipeline.
+  check(tw_rmsnorm_residual_host(input.values.data(), residual.values.data(), result.residual_out.values.data(),
+                                 result.output.values.data(), params.weight.data(), T, H, params.epsilon, TW_F32, 0,
+                                 nullptr),
         "rmsnorm_residual");
-  check(tw_memcpy(result.output.values.data(), d_out.ptr, nb, nullptr), "rmsnorm_residual: D2H");
-  check(tw_memcpy(result.residual_out.values.data(), d_rout.ptr, nb, nullptr), "rmsnorm_residual: D2H");
+  check(tw_device_synchronize(0), "rmsnorm_residual");
   return result;
 }
 

@@ -271,13 +271,22 @@ __global__ void __launch_bounds__(kBlock, 1) rownorm_kernel(const __grid_constan
           xr[k] = VT::mm_reduce(p.mc_in, e);
         } else {
           // Rank-ascending fp32 sum from 0.0f (proj/src/collectives.cpp:74-78).
+          // All ranks' loads are issued before the first add (memory-level
+          // parallelism); the sum itself keeps the reference's order.
+          Raw raw[kMaxRanks];
+#pragma unroll
+          for (int q = 0; q < kMaxRanks; ++q)
+            if (q < p.world) raw[q] = VT::load(p.peer_in[q], e);
 #pragma unroll
           for (int i = 0; i < N; ++i) xs[k][i] = 0.0f;
-          for (int q = 0; q < p.world; ++q) {
-            float f[N];
-            VT::unpack(VT::load(p.peer_in[q], e), f);
 #pragma unroll
-            for (int i = 0; i < N; ++i) xs[k][i] += f[i];
+          for (int q = 0; q < kMaxRanks; ++q) {
+            if (q < p.world) {
+              float f[N];
+              VT::unpack(raw[q], f);
+#pragma unroll
+              for (int i = 0; i < N; ++i) xs[k][i] += f[i];
+            }
           }
         }
         rr[k] = VT::load_stream(res_src, srow + static_cast<long long>(c) * N);

@@ -73,6 +73,25 @@ def test_k2_unaligned_pointers_take_the_scalar_path(cuda, orc):
     assert_abs_close(out.cpu().numpy(), want_out, 1e-5)
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+@pytest.mark.parametrize("T,H,chunk", [(100, 8192, 7), (1, 64, 0), (513, 4096, 64), (2048, 8192, 0), (37, 33, 5)])
+def test_k2_host_buffers_pipeline(cuda, orc, T, H, chunk, pinned):
+    """tw_rmsnorm_residual_host (chunked H2D | K2 | D2H) == the oracle."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    inp, res, w = norm_inputs(T + H + chunk, T, H)
+    inp, res = bf16_round(inp), bf16_round(res)
+    want_out, want_res = orc.rmsnorm_residual(inp, res, w)
+    hi = torch.from_numpy(inp).bfloat16()
+    hr = torch.from_numpy(res).bfloat16()
+    if pinned:
+        hi, hr = hi.pin_memory(), hr.pin_memory()
+    out, rout = tw.rmsnorm_residual_host(hi, hr, torch.from_numpy(w), chunk_rows=chunk)
+    torch.cuda.synchronize()
+    assert np.array_equal(rout.float().numpy(), bf16_round(want_res))
+    assert_bf16_close(out.float().numpy(), want_out)
+
+
 def test_k2_zero_input_normalizes_to_zero(cuda):
     import torch
     import paper_2505_11329_b200 as tw
