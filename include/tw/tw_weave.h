@@ -42,7 +42,9 @@ typedef struct tw_layer_spec {
 typedef enum tw_weave_mode {
   TW_MODE_FUSE_ONLY = 0,
   TW_MODE_WEAVE = 1,
-  TW_MODE_NO_COMM = 2
+  TW_MODE_NO_COMM = 2,
+  TW_MODE_UNFUSED = 3 /* baseline: attn -> add -> RMSNorm -> ffn -> add -> RMSNorm, one stream
+                         (the reference's Multimem chain, scheduler.cpp:153-164, at TP = 1) */
 } tw_weave_mode;
 
 /* Ops recorded by tw_weave_trace (the reference's OpKind, scheduler.hpp:12). */

@@ -181,6 +181,66 @@ tw_status fused(tw_weave* w, int64_t r0, int64_t n, int budget, cudaStream_t s) 
   return TW_OK;
 }
 
+// ---- unfused baseline boundary (NOT the product): residual add, then a
+// separate RMSNorm that re-reads r' -- the "AR + RMSNorm" row of the paper
+// without the AR (TP = 1), two launches and 6*S bytes instead of 4*S.
+__global__ void unfused_add_kernel(const uint4* __restrict__ a, uint4* __restrict__ r, long long nvec) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nvec;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const uint4 x = a[i];
+    uint4 y = r[i];
+    uint32_t* xs = reinterpret_cast<uint32_t*>(const_cast<uint4*>(&x));
+    uint32_t* ys = reinterpret_cast<uint32_t*>(&y);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float lo = __uint_as_float(xs[k] << 16) + __uint_as_float(ys[k] << 16);
+      const float hi = __uint_as_float(xs[k] & 0xffff0000u) + __uint_as_float(ys[k] & 0xffff0000u);
+      __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+      ys[k] = *reinterpret_cast<uint32_t*>(&v);
+    }
+    r[i] = y;
+  }
+}
+
+__global__ void unfused_rmsnorm_kernel(const uint16_t* __restrict__ r, uint16_t* __restrict__ x,
+                                       const float* __restrict__ w, int H) {
+  const uint16_t* row = r + static_cast<long long>(blockIdx.x) * H;
+  uint16_t* out = x + static_cast<long long>(blockIdx.x) * H;
+  float ss = 0.0f;
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    const float v = __uint_as_float(static_cast<uint32_t>(row[j]) << 16);
+    ss += v * v;
+  }
+  __shared__ float part[32];
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.0f;
+  for (int i = 0; i < static_cast<int>(blockDim.x >> 5); ++i) tot += part[i];
+  const float inv = rsqrtf(tot / H + 1e-5f);
+  for (int j = threadIdx.x; j < H; j += blockDim.x) {
+    const float v = __uint_as_float(static_cast<uint32_t>(row[j]) << 16);
+    __nv_bfloat16 o = __float2bfloat16_rn(v * inv * w[j]);
+    out[j] = *reinterpret_cast<uint16_t*>(&o);
+  }
+}
+
+tw_status unfused(tw_weave* w, int64_t r0, int64_t n, cudaStream_t s) {
+  if (n <= 0) return TW_OK;
+  const int64_t H = w->spec.hidden;
+  char* P = static_cast<char*>(w->P);
+  char* R = static_cast<char*>(w->R);
+  char* X = static_cast<char*>(w->X);
+  const long long nvec = n * H / 8;
+  unfused_add_kernel<<<static_cast<int>(std::min<long long>((nvec + 255) / 256, 148 * 16)), 256, 0, s>>>(
+      reinterpret_cast<const uint4*>(P + r0 * H * kBf16), reinterpret_cast<uint4*>(R + r0 * H * kBf16), nvec);
+  unfused_rmsnorm_kernel<<<static_cast<int>(n), 256, 0, s>>>(reinterpret_cast<const uint16_t*>(R + r0 * H * kBf16),
+                                                             reinterpret_cast<uint16_t*>(X + r0 * H * kBf16),
+                                                             w->wnorm, static_cast<int>(H));
+  CUDA_TRY(cudaGetLastError());
+  return TW_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -277,17 +337,17 @@ tw_status layer(tw_weave* w, int64_t T, int64_t ta, tw_weave_mode mode, int budg
     size_t id = op_begin(w, TW_OP_ATTENTION, 2, 0, cs);
     TW_TRY(attention(w, 0, T, 0));
     op_end(w, id, cs);
-    if (mode == TW_MODE_FUSE_ONLY) {
+    if (mode == TW_MODE_FUSE_ONLY || mode == TW_MODE_UNFUSED) {
       id = op_begin(w, TW_OP_FUSED, 2, 0, cs);
-      TW_TRY(fused(w, 0, T, 0, cs));
+      TW_TRY(mode == TW_MODE_UNFUSED ? unfused(w, 0, T, cs) : fused(w, 0, T, 0, cs));
       op_end(w, id, cs);
     }
     id = op_begin(w, TW_OP_FFN, 2, 0, cs);
     TW_TRY(ffn(w, 0, T));
     op_end(w, id, cs);
-    if (mode == TW_MODE_FUSE_ONLY) {
+    if (mode == TW_MODE_FUSE_ONLY || mode == TW_MODE_UNFUSED) {
       id = op_begin(w, TW_OP_FUSED, 2, 0, cs);
-      TW_TRY(fused(w, 0, T, 0, cs));
+      TW_TRY(mode == TW_MODE_UNFUSED ? unfused(w, 0, T, cs) : fused(w, 0, T, 0, cs));
       op_end(w, id, cs);
     }
     carry_a = edge(w);

@@ -10,7 +10,7 @@ from ctypes import CFUNCTYPE, POINTER, Structure, c_double, c_float, c_int, c_in
 from ._lib import check
 
 _LIBDIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
-MODES = {"fuseonly": 0, "tokenweave": 1, "nocomm": 2}
+MODES = {"fuseonly": 0, "tokenweave": 1, "nocomm": 2, "unfused": 3}
 OPS = {0: "attention", 1: "ffn", 2: "fused_ar_norm"}
 SPLITS = {0: "prefix", 1: "suffix", 2: "whole"}
 SPLIT_MODES = {0: "NoSplit", 1: "FusedOnly", 2: "Overlap"}
@@ -24,6 +24,22 @@ PRESETS = {
     "mixtral-8x22b": dict(hidden=6144, intermediate=16384, heads=48, kv_heads=8, head_dim=128, experts=8, top_k=2,
                           threshold=4096),
 }
+
+
+def timeline_json(events, latency_us: float) -> dict:
+    """Measured per-op timestamps of one layer in the reference's Timeline
+    schema (proj/src/scheduler.cpp:301-317): seconds, ids, depends_on edges
+    of build_layer_graph (:119-147 weave, :150-181 sequential chains)."""
+    n = len(events)
+    if n == 8:  # aa fa1 ab fb1 ffa fa2 ffb fb2
+        deps = [[], [0], [0], [2, 1], [1], [4, 3], [3], [6, 5]]
+    else:
+        deps = [[]] + [[i - 1] for i in range(1, n)]
+    t0 = min((e["start_us"] for e in events), default=0.0)
+    return {"iteration_latency": latency_us * 1e-6,
+            "events": [{"id": i, "op": e["op"], "split": e["split"], "stream": e["stream"],
+                        "start": (e["start_us"] - t0) * 1e-6, "end": (e["end_us"] - t0) * 1e-6,
+                        "depends_on": deps[i]} for i, e in enumerate(events)]}
 
 
 class LayerSpec(Structure):

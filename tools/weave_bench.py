@@ -1,10 +1,12 @@
-"""Measured weave vs sequential layer latency on one B200 (tw_weave.h runner).
+"""Measured weave vs sequential layers on one B200 (tw_weave.h runner).
 
-For each model/T: fuse-only (sequential), no-comm (lower bound), and the
-weave with (a) the analytic split of make_split_plan, (b) the equal split,
-(c) the measured Alg-1 sweep (smart_offset_sweep driven by real layer
-times).  GEMM shapes are one GPU's share at TP=8; the boundary op is K2.
-Prints one JSON object; --out writes it too.
+Per model / TP-shape / T: unfused sequential (add + RMSNorm as separate
+kernels), fuse-only sequential (K2), no-comm lower bound, and the weave with
+(a) the analytic split of make_split_plan, (b) the equal split, (c) the
+measured Alg-1 sweep (smart_offset_sweep over real layer times), over several
+boundary SM budgets.  `tp` sets the GEMM shapes (one GPU's share); the
+boundary op on one GPU is K2 over the split rows.  Writes one JSON document
+(--out) with the last layer's timeline in the reference's schema.
 """
 import argparse
 import json
@@ -15,6 +17,47 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def bench_case(weave, r, T, layers, budgets, ref, model, tp):
+    row = {"model": model, "tp_shapes": tp, "T": T}
+    row["unfused_us"] = r.run(T, "unfused", layers=layers)
+    row["fuseonly_us"] = r.run(T, "fuseonly", layers=layers)
+    row["nocomm_us"] = r.run(T, "nocomm", layers=layers)
+    a, b, off, mode = weave.make_split_plan(T, threshold=r.threshold)
+    row["plan"] = {"prefix": a, "suffix": b, "offset": off, "mode": weave.SPLIT_MODES[mode]}
+    best = (float("inf"), None)
+    for sms in budgets:
+        cands = {"equal": T // 2}
+        if mode == 2 and a != T // 2:
+            cands["analytic"] = a
+        for name, pa in cands.items():
+            us = r.run(T, "tokenweave", prefix=pa, boundary_sms=sms, layers=layers)
+            row[f"weave_{name}_sms{sms}_us"] = us
+            if us < best[0]:
+                best = (us, (pa, sms))
+    sms_best = best[1][1]
+    times = {}
+
+    def fwd(pa, pb):
+        times[pa] = r.run(T, "tokenweave", prefix=pa, boundary_sms=sms_best, layers=layers)
+        return times[pa]
+
+    off_sweep = weave.smart_offset_sweep(T, fwd)
+    row["alg1"] = {"boundary_sms": sms_best, "offset": off_sweep, "us": times[T // 2 + off_sweep],
+                   "grid_us": {str(k - T // 2): v for k, v in times.items()}}
+    if times[T // 2 + off_sweep] < best[0]:
+        best = (times[T // 2 + off_sweep], (T // 2 + off_sweep, sms_best))
+    row["weave_best_us"] = best[0]
+    row["weave_best_config"] = {"prefix": best[1][0], "boundary_sms": best[1][1]}
+    row["speedup_vs_unfused"] = row["unfused_us"] / best[0]
+    row["speedup_vs_fuseonly"] = row["fuseonly_us"] / best[0]
+    lat = r.run(T, "tokenweave", prefix=best[1][0], boundary_sms=best[1][1], layers=layers)
+    row["timeline"] = weave.timeline_json(r.trace(), lat)
+    if ref is not None and tp == 8:
+        row["reference_model_us"] = {m: 1e6 * ref.layer_latency("b200", model, T, m)
+                                     for m in ("multimem", "fuseonly", "tokenweave", "nocomm")}
+    return row
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--layers", type=int, default=6)
@@ -22,53 +65,26 @@ def main():
     ap.add_argument("--quick", action="store_true")
     args = ap.parse_args()
     from paper_2505_11329_b200 import weave
-    import oracle
     ref = None
     try:
+        import oracle  # reference simulator predictions ("predicted" column only)
         ref = oracle.RefLib()
     except Exception:
         pass
-    cases = [("llama-70b", [1024, 2048, 4096, 8192]), ("mixtral-8x22b", [4096, 8192])]
+    cases = [("llama-70b", 1, [1024, 2048, 4096, 8192], (16, 32, 64)),
+             ("llama-70b", 8, [1024, 2048, 4096, 8192], (16, 32, 64)),
+             ("mixtral-8x22b", 8, [4096, 8192], (16, 32, 64))]
     if args.quick:
-        cases = [("llama-70b", [2048, 8192])]
-    res = {"gemm_shapes": "per GPU at TP=8", "boundary_op": "K2 (tw_rmsnorm_residual) on the split rows",
+        cases = [("llama-70b", 1, [8192], (32,)), ("llama-70b", 8, [8192], (32,))]
+    res = {"device": "1x B200", "boundary_op": "K2 (tw_rmsnorm_residual) on the split rows",
+           "gemms": "cuBLAS bf16 (library load, not product); shapes = one GPU's share at tp_shapes",
            "layers_timed": args.layers, "rows": []}
-    for model, tokens in cases:
-        r = weave.LayerRunner(model, tp=8, max_tokens=max(tokens))
+    for model, tp, tokens, budgets in cases:
+        r = weave.LayerRunner(model, tp=tp, max_tokens=max(tokens))
         for T in tokens:
-            row = {"model": model, "T": T}
-            row["fuseonly_us"] = r.run(T, "fuseonly", layers=args.layers)
-            row["nocomm_us"] = r.run(T, "nocomm", layers=args.layers)
-            a, b, off, mode = weave.make_split_plan(T, threshold=r.threshold)
-            row["plan"] = {"prefix": a, "suffix": b, "offset": off, "mode": weave.SPLIT_MODES[mode]}
-            best = None
-            for sms in (8, 16, 32):
-                if mode == 2:
-                    us = r.run(T, "tokenweave", prefix=a, boundary_sms=sms, layers=args.layers)
-                    row[f"weave_analytic_sms{sms}_us"] = us
-                    best = us if best is None else min(best, us)
-                eq = r.run(T, "tokenweave", prefix=T // 2, boundary_sms=sms, layers=args.layers)
-                row[f"weave_equal_sms{sms}_us"] = eq
-                best = eq if best is None else min(best, eq)
-            # Alg. 1: measured sweep over the offset grid (boundary 16 SMs)
-            times = {}
-
-            def fwd(pa, pb):
-                times[pa] = r.run(T, "tokenweave", prefix=pa, boundary_sms=16, layers=args.layers)
-                return times[pa]
-
-            off_sweep = weave.smart_offset_sweep(T, fwd)
-            row["alg1_offset"] = off_sweep
-            row["alg1_us"] = times[T // 2 + off_sweep]
-            row["weave_best_us"] = min(best, row["alg1_us"])
-            row["speedup_vs_fuseonly"] = row["fuseonly_us"] / row["weave_best_us"]
-            r.run(T, "tokenweave", prefix=T // 2 + off_sweep, boundary_sms=16, layers=args.layers)
-            row["timeline"] = r.trace()
-            if ref is not None:
-                row["reference_model_us"] = {m: 1e6 * ref.layer_latency("b200", model, T, m)
-                                             for m in ("fuseonly", "tokenweave", "nocomm", "multimem")}
+            row = bench_case(weave, r, T, args.layers, budgets, ref, model, tp)
             res["rows"].append(row)
-            print(json.dumps({k: v for k, v in row.items() if k != "timeline"}), flush=True)
+            print(json.dumps({k: v for k, v in row.items() if k not in ("timeline",)}), flush=True)
         r.close()
     if args.out:
         with open(args.out, "w") as f:
