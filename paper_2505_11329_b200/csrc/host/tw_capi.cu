@@ -632,6 +632,15 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
   p.world = W;
   p.entry_target = static_cast<uint32_t>(comm->arrivals + per_barrier);
   p.exit_target = static_cast<uint32_t>(comm->arrivals + 2ull * per_barrier);
+  // Barrier poll bound (~2 s at the default) and the fault-injection hook of
+  // the timeout path: TW_FAULT_DROP_ARRIVAL_RANK=r makes rank r never signal,
+  // the B200 analogue of the reference's --inject-shard-fault
+  // (proj/src/commands.cpp:199-216).  A timed-out communicator is poisoned
+  // (its epoch mirror no longer matches the pads): destroy and recreate it.
+  const char* spin_env = std::getenv("TW_BARRIER_SPIN_LIMIT");
+  const char* drop_env = std::getenv("TW_FAULT_DROP_ARRIVAL_RANK");
+  p.spin_limit = spin_env ? std::atoll(spin_env) : (1ll << 25);
+  p.drop_arrival_rank = drop_env ? std::atoi(drop_env) : -1;
   for (int q = 0; q < W; ++q) {
     p.peer_in[q] = comm->ranks[q].buf[TW_BUF_INPUT];
     p.peer_out[q] = comm->ranks[q].buf[TW_BUF_OUTPUT];

@@ -68,7 +68,8 @@ struct RowParams {
   uint32_t* mc_pad;
   uint32_t entry_target, exit_target;
   int* err;
-  int skip_entry;  // 1: caller guarantees inputs are globally visible (tests)
+  long long spin_limit;   // barrier poll bound before the timeout flag is raised
+  int drop_arrival_rank;  // fault injection (tests): this rank never signals; -1 = none
 };
 
 constexpr unsigned kGatherResidual = 0x1u;
@@ -198,14 +199,19 @@ template <Xport X>
 __device__ __forceinline__ void rank_barrier(const RowParams& p, const RankSlot& s, uint32_t target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    if constexpr (X == Xport::Nvls) {
-      mm_red_release_add(p.mc_pad, 1u);
-    } else {
-      for (int q = 0; q < p.world; ++q) red_release_add(p.peer_pad[q], 1u);
+    // The CTA's prior writes are ordered before the arrival by bar.sync
+    // (cumulativity) + release semantics at system scope.
+    if (s.rank != p.drop_arrival_rank) {  // fault injection: a rank that never arrives
+      if constexpr (X == Xport::Nvls) {
+        mm_red_release_add(p.mc_pad, 1u);  // one op reaches every rank's pad
+      } else {
+        fence_acq_rel_sys();
+        for (int q = 0; q < p.world; ++q) red_relaxed_add(p.peer_pad[q], 1u);
+      }
     }
     long long spins = 0;
     while (static_cast<int>(ld_acquire(s.pad) - target) < 0) {
-      if (++spins > (1ll << 25)) {  // ~seconds: a rank was never launched
+      if (++spins > p.spin_limit) {  // bounded: a rank was never launched / died
         atomicExch(p.err, 1);
         break;
       }
@@ -237,7 +243,7 @@ __global__ void __launch_bounds__(kBlock, 1) rownorm_kernel(const __grid_constan
   const long long H = p.H;
 
   if constexpr (X != Xport::Local) {
-    if (!p.skip_entry) rank_barrier<X>(p, s, p.entry_target);
+    rank_barrier<X>(p, s, p.entry_target);
   }
 
   long long row0, row1;

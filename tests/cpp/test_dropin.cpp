@@ -7,6 +7,7 @@
 //
 // Cases follow proj/tests/test_numerics.cpp, test_collectives.cpp,
 // test_splitter.cpp and acceptance.cpp check 1 (cited per case).
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -218,12 +219,23 @@ void gpu_cases() {
   const TokenMatrix b = fused_allreduce_rmsnorm(par, unit_norm(24), s53, true);
   CHECK(a.values == b.values);
   for (int r = 0; r < 8; ++r) CHECK(seq.residual_shards[r].values == par.residual_shards[r].values);
-  // acceptance.cpp:37-86 (slice of the grid: 1e-5 vs the unfused chain)
+}
+
+// acceptance.cpp:37-86 -- the fused op vs the unfused chain over the
+// acceptance grid (full grid: N{2,4,8} x T{1,3,17,256,1024} x H{16,64,1024}
+// x 50 seeds = 2250 instances, <= 1e-5, < 60 s).
+void acceptance_cases(bool full) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const std::vector<std::int64_t> token_grid =
+      full ? std::vector<std::int64_t>{1, 3, 17, 256, 1024} : std::vector<std::int64_t>{1, 3, 17, 256};
+  const int seeds = full ? 50 : 2;
   double max_err = 0;
+  long instances = 0;
   for (int world : {2, 4, 8})
-    for (std::int64_t tokens : {1, 3, 17, 256})
+    for (std::int64_t tokens : token_grid)
       for (std::int64_t hidden : {16, 64, 1024})
-        for (int seed = 0; seed < 2; ++seed) {
+        for (int seed = 0; seed < seeds; ++seed) {
+          ++instances;
           std::mt19937_64 r2((std::uint64_t(world) << 48) ^ (std::uint64_t(tokens) << 24) ^
                              (std::uint64_t(hidden) << 8) ^ std::uint64_t(seed));
           std::uniform_real_distribution<float> d(-1.f, 1.f);
@@ -249,16 +261,24 @@ void gpu_cases() {
           for (size_t i = 0; i < fused.values.size(); ++i)
             max_err = std::max(max_err, double(std::abs(fused.values[i] - orc.output.values[i])));
         }
-  std::printf("acceptance-slice max_abs_err=%.3g\n", max_err);
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::printf("acceptance%s instances=%ld max_abs_err=%.3g runtime=%.1fs\n", full ? "" : "-slice", instances, max_err,
+              secs);
   CHECK(max_err <= 1e-5);
+  if (full) CHECK(secs < 60.0);
 }
 
 }  // namespace
 
+// usage: test_dropin host | gpu | acceptance
 int main(int argc, char** argv) {
-  const bool gpu = argc > 1 && std::strcmp(argv[1], "gpu") == 0;
+  const std::string mode = argc > 1 ? argv[1] : "host";
   host_cases();
-  if (gpu) gpu_cases();
-  std::printf("%s: %d passed, %d failed\n", gpu ? "gpu" : "host", g_pass, g_fail);
+  if (mode == "gpu") {
+    gpu_cases();
+    acceptance_cases(false);
+  }
+  if (mode == "acceptance") acceptance_cases(true);
+  std::printf("%s: %d passed, %d failed\n", mode.c_str(), g_pass, g_fail);
   return g_fail ? 1 : 0;
 }

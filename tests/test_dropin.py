@@ -32,3 +32,12 @@ def test_dropin_gpu_cases():
     out = run("gpu")
     assert "0 failed" in out
     print(out)
+
+
+@pytest.mark.gpu
+def test_dropin_acceptance_check1_full_grid():
+    """proj/tests/acceptance.cpp check 1 on the drop-in: 2250 instances,
+    fused vs unfused chain <= 1e-5, < 60 s."""
+    out = run("acceptance")
+    assert "instances=2250" in out and "0 failed" in out, out
+    print(out)

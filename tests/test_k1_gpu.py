@@ -172,6 +172,34 @@ def test_k1_repeated_launches_and_budgets(cuda, orc):
     comm.close()
 
 
+def test_k1_barrier_timeout_fault_injection(cuda, monkeypatch):
+    """A rank that never arrives must not hang the GPU: the bounded spin raises
+    the timeout flag and tw_comm_check reports BarrierTimeout."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    W, T, H = 4, 64, 256
+    comm = tw.Communicator(W, [0] * W, T * H * 2, tw.TW_TRANSPORT_PEER)
+    shards = [torch.zeros(T // W, H, device="cuda", dtype=torch.bfloat16) for _ in range(W)]
+    w = [torch.ones(H, device="cuda")] * W
+    comm.fused_allreduce_rmsnorm(T, H, shards, w, sm_budget=2)
+    torch.cuda.synchronize()
+    comm.check()  # healthy
+    monkeypatch.setenv("TW_FAULT_DROP_ARRIVAL_RANK", "2")
+    monkeypatch.setenv("TW_BARRIER_SPIN_LIMIT", "20000")
+    comm.fused_allreduce_rmsnorm(T, H, shards, w, sm_budget=2)
+    torch.cuda.synchronize()
+    with pytest.raises(tw.BarrierTimeout):
+        comm.check()
+    comm.close()
+    monkeypatch.delenv("TW_FAULT_DROP_ARRIVAL_RANK")
+    monkeypatch.delenv("TW_BARRIER_SPIN_LIMIT")
+    fresh = tw.Communicator(W, [0] * W, T * H * 2, tw.TW_TRANSPORT_PEER)
+    fresh.fused_allreduce_rmsnorm(T, H, shards, w, sm_budget=2)
+    torch.cuda.synchronize()
+    fresh.check()  # a recreated communicator is healthy again
+    fresh.close()
+
+
 def test_k3_allreduce_baseline(cuda, orc):
     import torch
     import paper_2505_11329_b200 as tw
