@@ -150,9 +150,10 @@ TW_API tw_status tw_fused_allreduce_rmsnorm_group(tw_comm_t comm, int64_t T, int
  * creates the NVLS multicast object and shares it by POSIX fd over an
  * abstract Unix socket.  Collective per-rank calls must be made in the same
  * order with the same shapes on every rank (the signal-pad epochs are
- * host-tracked).  Transport is always NVLS. */
+ * host-tracked).  transport: NVLS, PEER (cudaIpc-mapped peer buffers, NVLink
+ * P2P), or AUTO = NVLS with a collective fallback to PEER. */
 TW_API tw_status tw_comm_create_mp(int world, int rank, int device, size_t buffer_bytes, const char* rendezvous_id,
-                                   tw_comm_t* out);
+                                   tw_transport transport, tw_comm_t* out);
 /* K1 for the rank this process owns (multi-process communicators). */
 TW_API tw_status tw_fused_allreduce_rmsnorm(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset,
                                             const int64_t* shard_ranges, void* residual_shard, const float* weight,

@@ -91,7 +91,7 @@ _SIGNATURES = [
     ("tw_memcpy", c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
     ("tw_device_synchronize", c_int, [c_int]),
     ("tw_comm_check", c_int, [c_void_p]),
-    ("tw_comm_create_mp", c_int, [c_int, c_int, c_int, c_size_t, c_char_p, POINTER(c_void_p)]),
+    ("tw_comm_create_mp", c_int, [c_int, c_int, c_int, c_size_t, c_char_p, c_int, POINTER(c_void_p)]),
     ("tw_fused_allreduce_rmsnorm", c_int,
      [c_void_p, c_int64, c_int64, c_int64, POINTER(c_int64), c_void_p, c_void_p, c_float, c_int, c_int, c_uint,
       c_void_p]),

@@ -222,6 +222,10 @@ static tw_status create_nvls(tw_comm* c) {
 void destroy_comm(tw_comm* c) {
   const Driver& d = driver();
   for (RankBuffers& rb : c->ranks) {
+    if (rb.ipc_base) {  // a peer's memory imported by this process
+      cudaIpcCloseMemHandle(rb.ipc_base);
+      continue;
+    }
     if (!rb.buf[0] && !rb.phys && !rb.uc_base && !rb.mc_base) continue;  // not owned by this process
     cudaSetDevice(rb.device);
     cudaDeviceSynchronize();

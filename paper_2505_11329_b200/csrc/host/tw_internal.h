@@ -56,6 +56,7 @@ struct RankBuffers {
   CUmemGenericAllocationHandle phys = 0;
   CUdeviceptr uc_base = 0, mc_base = 0;
   bool owns_cuda_malloc = false;
+  void* ipc_base = nullptr;  // multi-process PEER: a peer's allocation opened via cudaIpcOpenMemHandle
 };
 
 }  // namespace tw

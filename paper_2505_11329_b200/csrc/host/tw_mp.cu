@@ -122,6 +122,24 @@ class Rendezvous {
     return true;
   }
 
+  // Every rank contributes n bytes; all ranks receive the rank-ordered table.
+  bool allgather(const void* mine, size_t n, void* all, std::string* err) {
+    char* table = static_cast<char*>(all);
+    std::memcpy(table + static_cast<size_t>(rank_) * n, mine, n);
+    if (world_ == 1) return true;
+    if (rank_ == 0) {
+      for (int r = 1; r < world_; ++r)
+        if (!read_all(peers_[r], table + static_cast<size_t>(r) * n, n))
+          return fail_msg(err, "rendezvous: allgather read failed");
+      for (int r = 1; r < world_; ++r)
+        if (!write_all(peers_[r], table, n * world_)) return fail_msg(err, "rendezvous: allgather write failed");
+      return true;
+    }
+    if (!write_all(peers_[0], mine, n) || !read_all(peers_[0], table, n * world_))
+      return fail_msg(err, "rendezvous: allgather with rank 0 failed");
+    return true;
+  }
+
  private:
   static bool fail_msg(std::string* err, const char* m) {
     *err = m;
@@ -268,6 +286,46 @@ tw_status create_nvls_mp(tw_comm* c, int rank, const char* id) {
   return TW_OK;
 }
 
+// PEER transport across processes: each rank cudaMallocs its buffers and
+// shares a cudaIpcMemHandle; peers map it (NVLink P2P loads/stores).
+tw_status create_peer_mp(tw_comm* c, int rank, const std::string& id) {
+  RankBuffers& rb = c->ranks[rank];
+  c->region = round_up(std::max<size_t>(c->bytes, 1), 256);
+  c->total = 3 * c->region + 4096;
+  char* base = nullptr;
+  cudaError_t e = cudaMalloc(&base, c->total);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(comm buffers)");
+  rb.owns_cuda_malloc = true;
+  for (int b = 0; b < 3; ++b) rb.buf[b] = base + b * c->region;
+  rb.pad = reinterpret_cast<uint32_t*>(base + 3 * c->region);
+  rb.err = reinterpret_cast<int*>(base + 3 * c->region + 2048);
+  e = cudaMemset(base + 3 * c->region, 0, 4096);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return cuda_fail(e, "zero signal pad");
+  cudaIpcMemHandle_t mine;
+  e = cudaIpcGetMemHandle(&mine, base);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+  Rendezvous rv(id, c->world, rank);
+  std::string err;
+  if (!rv.connect_all(&err)) return fail(TW_ERR_CONFIG, err);
+  std::vector<cudaIpcMemHandle_t> table(c->world);
+  if (!rv.allgather(&mine, sizeof(mine), table.data(), &err)) return fail(TW_ERR_CONFIG, err);
+  for (int q = 0; q < c->world; ++q) {
+    if (q == rank) continue;
+    void* peer = nullptr;
+    e = cudaIpcOpenMemHandle(&peer, table[q], cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle (no P2P path between the GPUs?)");
+    RankBuffers& pb = c->ranks[q];
+    pb.ipc_base = peer;
+    char* pbase = static_cast<char*>(peer);
+    for (int b = 0; b < 3; ++b) pb.buf[b] = pbase + b * c->region;
+    pb.pad = reinterpret_cast<uint32_t*>(pbase + 3 * c->region);
+    pb.err = reinterpret_cast<int*>(pbase + 3 * c->region + 2048);
+  }
+  if (!rv.barrier(&err)) return fail(TW_ERR_CONFIG, err);  // every pad zeroed and mapped before any signal
+  return TW_OK;
+}
+
 }  // namespace
 }  // namespace tw
 
@@ -276,7 +334,7 @@ using namespace tw;
 extern "C" {
 
 tw_status tw_comm_create_mp(int world, int rank, int device, size_t buffer_bytes, const char* rendezvous_id,
-                            tw_comm_t* out) {
+                            tw_transport transport, tw_comm_t* out) {
   clear_error();
   if (!out) return fail(TW_ERR_CONFIG, "comm_create_mp: null output");
   *out = nullptr;
@@ -289,21 +347,41 @@ tw_status tw_comm_create_mp(int world, int rank, int device, size_t buffer_bytes
   int prev = 0;
   cudaGetDevice(&prev);
   cudaSetDevice(device);
-  tw_comm* c = new tw_comm();
-  c->world = world;
-  c->bytes = buffer_bytes;
-  c->transport = TW_TRANSPORT_NVLS;
-  c->local_rank = rank;
-  c->ranks.resize(world);
-  c->ranks[rank].device = device;
-  const tw_status st = create_nvls_mp(c, rank, rendezvous_id);
-  if (st != TW_OK) {
-    const std::string why = tw_last_error();
-    destroy_comm(c);
-    cudaSetDevice(prev);
-    return fail(st, why);
+  auto fresh = [&](tw_transport t) {
+    tw_comm* c = new tw_comm();
+    c->world = world;
+    c->bytes = buffer_bytes;
+    c->transport = t;
+    c->local_rank = rank;
+    c->ranks.resize(world);
+    c->ranks[rank].device = device;
+    return c;
+  };
+  tw_comm* c = nullptr;
+  tw_status st = TW_ERR_UNSUPPORTED;
+  std::string why;
+  if (transport != TW_TRANSPORT_PEER) {
+    c = fresh(TW_TRANSPORT_NVLS);
+    st = create_nvls_mp(c, rank, rendezvous_id);
+    if (st != TW_OK) {
+      why = tw_last_error();
+      destroy_comm(c);
+      c = nullptr;
+    }
+  }
+  // AUTO: every rank fails NVLS together (each failure closes the rendezvous
+  // sockets its peers block on), then all retry on the PEER transport.
+  if (st != TW_OK && transport != TW_TRANSPORT_NVLS) {
+    c = fresh(TW_TRANSPORT_PEER);
+    st = create_peer_mp(c, rank, std::string(rendezvous_id) + ":peer");
+    if (st != TW_OK) {
+      why += (why.empty() ? "" : "; ") + std::string(tw_last_error());
+      destroy_comm(c);
+      c = nullptr;
+    }
   }
   cudaSetDevice(prev);
+  if (st != TW_OK) return fail(st, why);
   *out = c;
   return TW_OK;
 }

@@ -52,7 +52,11 @@ def run_tp(args):
     gather = bool(getattr(args, "gather_residual", False))
     rid = rendezvous_id(dist)
     h = ctypes.c_void_p()
-    _lib.check(_lib.lib.tw_comm_create_mp(world, rank, local, T * H * 2, rid.encode(), ctypes.byref(h)))
+    _lib.check(_lib.lib.tw_comm_create_mp(world, rank, local, T * H * 2, rid.encode(), _lib.TW_TRANSPORT_AUTO,
+                                          ctypes.byref(h)))
+    wsz, tr, nb = ctypes.c_int(), ctypes.c_int(), ctypes.c_size_t()
+    _lib.check(_lib.lib.tw_comm_info(h, ctypes.byref(wsz), ctypes.byref(tr), ctypes.byref(nb)))
+    transport = _lib.TRANSPORT_NAMES[tr.value]
     ranges = tw.token_shard_map(T, world)
     b, e = ranges[rank]
     flat = (ctypes.c_int64 * (2 * world))(*[v for rg in ranges for v in rg])
@@ -102,6 +106,7 @@ def run_tp(args):
             "dtype": "bf16", "data": "synthetic U(-0.5,0.5) bf16 partial sums",
             "config": {"workload": f"TP={world} fused AllReduce+residual+RMSNorm (K1, NVLS), {T} tok x {H} hid bf16",
                        "tokens": T, "hidden": H, "tp": world, "sm_budget": budget, "gather_residual": gather,
+                       "transport": transport,
                        "l2": "inputs in HBM; NVLink-bound"},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": 900.0, "unit": "GB/s",
                          "frac": round(achieved / 900.0, 4), "peak_kind": "nominal per direction",
