@@ -45,9 +45,15 @@ def run_tp(args):
 
     world = int(os.environ.get("WORLD_SIZE", args.gpus))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    ndev = torch.cuda.device_count()
+    local = int(os.environ.get("LOCAL_RANK", rank)) % max(ndev, 1)
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if ndev >= world:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        red_device = "cuda"
+    else:  # ranks share GPUs (test topologies): NCCL refuses duplicate devices
+        dist.init_process_group("gloo")
+        red_device = None
     T, H = args.tokens, args.hidden
     gather = bool(getattr(args, "gather_residual", False))
     rid = rendezvous_id(dist)
@@ -95,7 +101,7 @@ def run_tp(args):
     _lib.check(_lib.lib.tw_comm_check(h))
     times = [s.elapsed_time(x) for s, x in zip(starts, ends)]
     us_local = 1e3 * sum(times) / len(times)
-    us = max_over_ranks(us_local, dist, device="cuda")
+    us = max_over_ranks(us_local, dist, device=red_device)
     nvl = algorithmic_nvlink_bytes(T, H, world, gather)
     achieved = nvl / (us * 1e-6) / 1e9
     if rank == 0:
@@ -104,7 +110,8 @@ def run_tp(args):
             "value": round(us, 3), "unit": "us", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(us / 1e3, 6), "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "bf16", "data": "synthetic U(-0.5,0.5) bf16 partial sums",
-            "config": {"workload": f"TP={world} fused AllReduce+residual+RMSNorm (K1, NVLS), {T} tok x {H} hid bf16",
+            "config": {"workload": f"TP={world} fused AllReduce+residual+RMSNorm (K1, {transport.upper()}), "
+                                   f"{T} tok x {H} hid bf16",
                        "tokens": T, "hidden": H, "tp": world, "sm_budget": budget, "gather_residual": gather,
                        "transport": transport,
                        "l2": "inputs in HBM; NVLink-bound"},
