@@ -131,6 +131,9 @@ def reference_rmsnorm_ms(T, H, threads, iters):
 def run_reference_arm(args):
     if int(os.environ.get("RANK", "0")) != 0:
         return 0
+    world = max(args.gpus, int(os.environ.get("WORLD_SIZE", "1")))
+    if world > 1:
+        return run_reference_arm_tp(args, world)
     T, H = args.tokens, args.hidden
     threads = os.cpu_count() or 1
     for _ in range(args.warmup):
@@ -149,6 +152,39 @@ def run_reference_arm(args):
         "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": f"full workload every step ({T}x{H} fp32): token rows chunked over {threads} "
                                    f"threads, each calling weavesim::rmsnorm_residual; wall {wall:.1f}s"},
+        "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_reference_arm_tp(args, world):
+    """TP = N config: the reference's own fused_allreduce_rmsnorm
+    (proj/src/collectives.cpp:157-182) with N in-process ranks on N
+    std::threads (parallel=true, its fastest mode), including its validation.
+    Each step is a bounded row sample scaled to the full T."""
+    import oracle  # --impl reference leg only
+    ref = oracle.RefLib()
+    T, H = args.tokens, args.hidden
+    sample_T = min(T, 1024)
+    for _ in range(args.warmup):
+        ref.time_fused(world, sample_T, H, True, 1)
+    t0 = time.perf_counter()
+    ms = [ref.time_fused(world, sample_T, H, True, 1) * T / sample_T for _ in range(args.steps)]
+    wall = time.perf_counter() - t0
+    us = 1e3 * sum(ms) / len(ms)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(us / 1e3, 3), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic U(-1,1) inputs, unit weight",
+        "config": {"workload": f"TP={world} fused AllReduce+residual+RMSNorm, {T} tok x {H} hid "
+                               f"(reference CPU path, {world} simulated ranks)", "tokens": T, "hidden": H,
+                   "tp": world},
+        "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": world, "kind": "reference",
+                         "sample": f"{sample_T}-token sample per step ({world} ranks x {sample_T}x{H} fp32, "
+                                   f"parallel=true: one std::thread per rank), scaled x{T / sample_T:g}; "
+                                   f"wall {wall:.1f}s"},
         "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
