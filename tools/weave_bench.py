@@ -46,11 +46,21 @@ def bench_case(weave, r, T, layers, budgets, ref, model, tp):
                    "grid_us": {str(k - T // 2): v for k, v in times.items()}}
     if times[T // 2 + off_sweep] < best[0]:
         best = (times[T // 2 + off_sweep], (T // 2 + off_sweep, sms_best))
+    # SM partition for the GEMMs (cublasSetSmCountTarget), the reference's SM tax
+    part = {}
+    for sms in budgets:
+        us = r.run(T, "tokenweave", prefix=best[1][0], boundary_sms=sms, gemm_sms=148 - sms, layers=layers)
+        part[str(sms)] = us
+        if us < best[0]:
+            best = (us, (best[1][0], sms, 148 - sms))
+    row["weave_partitioned_us"] = part
     row["weave_best_us"] = best[0]
-    row["weave_best_config"] = {"prefix": best[1][0], "boundary_sms": best[1][1]}
+    row["weave_best_config"] = {"prefix": best[1][0], "boundary_sms": best[1][1],
+                                "gemm_sms": best[1][2] if len(best[1]) > 2 else 0}
     row["speedup_vs_unfused"] = row["unfused_us"] / best[0]
     row["speedup_vs_fuseonly"] = row["fuseonly_us"] / best[0]
-    lat = r.run(T, "tokenweave", prefix=best[1][0], boundary_sms=best[1][1], layers=layers)
+    lat = r.run(T, "tokenweave", prefix=best[1][0], boundary_sms=best[1][1],
+                gemm_sms=best[1][2] if len(best[1]) > 2 else 0, layers=layers)
     row["timeline"] = weave.timeline_json(r.trace(), lat)
     if ref is not None and tp == 8:
         row["reference_model_us"] = {m: 1e6 * ref.layer_latency("b200", model, T, m)
