@@ -245,14 +245,6 @@ void destroy_comm(tw_comm* c) {
   delete c;
 }
 
-// ---- shared launch preparation --------------------------------------------------------
-
-struct Prep {
-  RowPlan plan;
-  bool bf16;
-  Xport x;
-  int budget;
-};
 
 }  // namespace tw
 
