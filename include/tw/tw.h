@@ -118,6 +118,8 @@ TW_API tw_status tw_comm_create(int world, const int* devices, size_t buffer_byt
                          tw_comm_t* out);
 TW_API tw_status tw_comm_destroy(tw_comm_t comm);
 TW_API tw_status tw_comm_info(tw_comm_t comm, int* world, tw_transport* transport, size_t* buffer_bytes);
+/* The rank this process owns and its device (rank = -1: single-process comm). */
+TW_API tw_status tw_comm_local_rank(tw_comm_t comm, int* rank, int* device);
 TW_API tw_status tw_comm_buffer(tw_comm_t comm, int rank, tw_buffer which, void** device_ptr);
 /* Multicast (NVLS) address of a buffer; TW_ERR_UNSUPPORTED on PEER comms. */
 TW_API tw_status tw_comm_multicast_buffer(tw_comm_t comm, int rank, tw_buffer which, void** device_ptr);

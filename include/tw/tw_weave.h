@@ -53,6 +53,14 @@ typedef enum tw_weave_op { TW_OP_ATTENTION = 0, TW_OP_FFN = 1, TW_OP_FUSED = 2 }
 typedef struct tw_weave* tw_weave_t;
 
 TW_API tw_status tw_weave_create(const tw_layer_spec* spec, int64_t max_tokens, int device, tw_weave_t* out);
+/* TP >= 2 with one process per GPU: `comm` is a multi-process communicator
+ * (tw_comm_create_mp, buffers >= max_tokens*hidden*2 B) and spec->tp its world
+ * size.  The GEMMs write their partial sums into this rank's INPUT buffer and
+ * the boundary op is K1 (tw_fused_allreduce_rmsnorm) on the split's rows;
+ * TW_MODE_UNFUSED runs the K3 AllReduce + separate add/RMSNorm instead.
+ * Every rank must issue the same tw_weave_run calls. */
+TW_API tw_status tw_weave_create_tp(const tw_layer_spec* spec, int64_t max_tokens, tw_comm_t comm,
+                                    tw_weave_t* out);
 TW_API tw_status tw_weave_destroy(tw_weave_t w);
 
 /* Runs `layers` chained layers of T tokens (prefix_tokens used by WEAVE) and

@@ -80,6 +80,7 @@ _SIGNATURES = [
     ("tw_comm_create", c_int, [c_int, POINTER(c_int), c_size_t, c_int, POINTER(c_void_p)]),
     ("tw_comm_destroy", c_int, [c_void_p]),
     ("tw_comm_info", c_int, [c_void_p, POINTER(c_int), POINTER(c_int), POINTER(c_size_t)]),
+    ("tw_comm_local_rank", c_int, [c_void_p, POINTER(c_int), POINTER(c_int)]),
     ("tw_comm_buffer", c_int, [c_void_p, c_int, c_int, POINTER(c_void_p)]),
     ("tw_comm_multicast_buffer", c_int, [c_void_p, c_int, c_int, POINTER(c_void_p)]),
     ("tw_fused_allreduce_rmsnorm_group", c_int,

@@ -464,6 +464,14 @@ tw_status tw_comm_info(tw_comm_t comm, int* world, tw_transport* transport, size
   return TW_OK;
 }
 
+tw_status tw_comm_local_rank(tw_comm_t comm, int* rank, int* device) {
+  clear_error();
+  if (!comm) return fail(TW_ERR_CONFIG, "comm_local_rank: null communicator");
+  if (rank) *rank = comm->local_rank;
+  if (device) *device = comm->ranks[comm->local_rank < 0 ? 0 : comm->local_rank].device;
+  return TW_OK;
+}
+
 tw_status tw_comm_buffer(tw_comm_t comm, int rank, tw_buffer which, void** device_ptr) {
   clear_error();
   if (!comm || !device_ptr) return fail(TW_ERR_CONFIG, "comm_buffer: null argument");

@@ -71,6 +71,13 @@ struct tw_weave {
   cudaEvent_t t0 = nullptr;
   std::vector<cudaEvent_t> dag;  // edge events
   size_t dag_used = 0;
+  // TP >= 2 (multi-process communicator): P is this rank's symmetric INPUT,
+  // the fused op writes the replicated normed hidden into OUTPUT, R holds
+  // this rank's residual shard rows of every split (full [T,H] addressing).
+  tw_comm_t comm = nullptr;
+  int rank = 0, world = 1;
+  void* X_local = nullptr;  // TP=1 / unfused-baseline hidden buffer
+  void* X_comm = nullptr;   // comm OUTPUT
 };
 
 namespace {
@@ -168,14 +175,26 @@ tw_status ffn(tw_weave* w, int64_t r0, int64_t n) {
   return TW_OK;
 }
 
-// Layer-boundary op on rows [r0, r0+n): K2 (tp == 1) reading the partial sums
-// P, updating the residual R in place and writing the normed hidden X.
+// Layer-boundary op on rows [r0, r0+n).
+//  * single device: K2 reading the partial sums P, updating the residual R in
+//    place and writing the normed hidden X;
+//  * TP >= 2: K1 on rows [r0, r0+n) of the communicator's symmetric buffers
+//    (token_offset = r0): the split's token_shard_map gives this rank's rows,
+//    whose residual lives at R + (r0 + b_rank) * H; the replicated output
+//    lands in every rank's OUTPUT (= X).
 tw_status fused(tw_weave* w, int64_t r0, int64_t n, int budget, cudaStream_t s) {
   if (n <= 0) return TW_OK;
   const int64_t H = w->spec.hidden;
   char* P = static_cast<char*>(w->P);
   char* R = static_cast<char*>(w->R);
   char* X = static_cast<char*>(w->X);
+  if (w->comm) {
+    int64_t ranges[16];
+    TW_TRY(tw_token_shard_map(n, w->world, ranges));
+    char* shard = R + (r0 + ranges[2 * w->rank]) * H * kBf16;
+    TW_TRY(tw_fused_allreduce_rmsnorm(w->comm, n, H, r0, ranges, shard, w->wnorm, 1e-5f, TW_BF16, budget, 0u, s));
+    return TW_OK;
+  }
   TW_TRY(tw_rmsnorm_residual(P + r0 * H * kBf16, R + r0 * H * kBf16, R + r0 * H * kBf16, X + r0 * H * kBf16,
                              w->wnorm, n, H, 1e-5f, TW_BF16, budget, s));
   return TW_OK;
@@ -231,6 +250,13 @@ tw_status unfused(tw_weave* w, int64_t r0, int64_t n, cudaStream_t s) {
   char* P = static_cast<char*>(w->P);
   char* R = static_cast<char*>(w->R);
   char* X = static_cast<char*>(w->X);
+  if (w->comm) {
+    // TP >= 2: the one-shot AllReduce (K3) INPUT -> OUTPUT first; the residual
+    // is replicated (every rank adds and normalises all rows), as in an
+    // unfused engine.
+    TW_TRY(tw_allreduce(w->comm, n, H, r0, TW_BF16, 0, s));
+    P = static_cast<char*>(w->X_comm);
+  }
   const long long nvec = n * H / 8;
   unfused_add_kernel<<<static_cast<int>(std::min<long long>((nvec + 255) / 256, 148 * 16)), 256, 0, s>>>(
       reinterpret_cast<const uint4*>(P + r0 * H * kBf16), reinterpret_cast<uint4*>(R + r0 * H * kBf16), nvec);
@@ -245,7 +271,25 @@ tw_status unfused(tw_weave* w, int64_t r0, int64_t n, cudaStream_t s) {
 
 extern "C" {
 
+static tw_status weave_create(const tw_layer_spec* spec, int64_t max_tokens, int device, tw_comm_t comm,
+                              tw_weave_t* out);
+
 tw_status tw_weave_create(const tw_layer_spec* spec, int64_t max_tokens, int device, tw_weave_t* out) {
+  return weave_create(spec, max_tokens, device, nullptr, out);
+}
+
+tw_status tw_weave_create_tp(const tw_layer_spec* spec, int64_t max_tokens, tw_comm_t comm, tw_weave_t* out) {
+  if (!comm) return werr(TW_ERR_CONFIG, "weave_create_tp: null communicator");
+  int rank = -1, device = 0, world = 0;
+  TW_TRY(tw_comm_local_rank(comm, &rank, &device));
+  TW_TRY(tw_comm_info(comm, &world, nullptr, nullptr));
+  if (rank < 0) return werr(TW_ERR_CONFIG, "weave_create_tp: needs a multi-process communicator (one rank here)");
+  if (!spec || spec->tp != world) return werr(TW_ERR_CONFIG, "weave_create_tp: spec.tp must equal the world size");
+  return weave_create(spec, max_tokens, device, comm, out);
+}
+
+static tw_status weave_create(const tw_layer_spec* spec, int64_t max_tokens, int device, tw_comm_t comm,
+                              tw_weave_t* out) {
   if (!spec || !out) return werr(TW_ERR_CONFIG, "weave_create: null argument");
   *out = nullptr;
   const tw_layer_spec& sp = *spec;
@@ -268,8 +312,8 @@ tw_status tw_weave_create(const tw_layer_spec* spec, int64_t max_tokens, int dev
     void** p;
     size_t bytes;
   } allocs[] = {
-      {&w->X, size_t(T * H * kBf16)},
-      {&w->P, size_t(T * H * kBf16)},
+      {&w->X_local, size_t(T * H * kBf16)},
+      {&w->P, size_t(comm ? 16 : T * H * kBf16)},
       {&w->R, size_t(T * H * kBf16)},
       {&w->QKV, size_t(T * std::max(w->qkvw, hd) * kBf16) + size_t(T * d * kBf16)},
       {&w->S, size_t(w->hg * T * T * kBf16)},
@@ -290,6 +334,21 @@ tw_status tw_weave_create(const tw_layer_spec* spec, int64_t max_tokens, int dev
       return werr(TW_ERR_CUDA, std::string("weave_create: cudaMalloc: ") + cudaGetErrorString(e));
     }
   }
+  w->X = w->X_local;
+  if (comm) {
+    size_t bytes = 0;
+    TW_TRY(tw_comm_info(comm, &w->world, nullptr, &bytes));
+    TW_TRY(tw_comm_local_rank(comm, &w->rank, nullptr));
+    if (bytes < size_t(T * H * kBf16)) {
+      tw_weave_destroy(w);
+      return werr(TW_ERR_DIMENSION, "weave_create_tp: communicator buffers smaller than max_tokens x hidden");
+    }
+    cudaFree(w->P);
+    TW_TRY(tw_comm_buffer(comm, w->rank, TW_BUF_INPUT, &w->P));      // GEMMs write partial sums here
+    TW_TRY(tw_comm_buffer(comm, w->rank, TW_BUF_OUTPUT, &w->X_comm));  // K1 writes the normed hidden here
+    w->comm = comm;
+    w->X = w->X_comm;
+  }
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   CUDA_TRY(cudaStreamCreateWithPriority(&w->compute, cudaStreamNonBlocking, lo));
@@ -305,7 +364,8 @@ tw_status tw_weave_destroy(tw_weave_t w) {
   if (!w) return TW_OK;
   cudaSetDevice(w->device);
   cudaDeviceSynchronize();
-  void* bufs[] = {w->X, w->P, w->R, w->QKV, w->S, w->A, w->F, w->PE, w->Wqkv, w->Wo, w->Wup, w->Wdown, w->wnorm};
+  void* bufs[] = {w->X_local, w->comm ? nullptr : w->P, w->R, w->QKV, w->S, w->A, w->F, w->PE, w->Wqkv, w->Wo,
+                  w->Wup, w->Wdown, w->wnorm};  // P / X_comm belong to the communicator in TP mode
   for (void* b : bufs)
     if (b) cudaFree(b);
   for (Ev& e : w->pool) {
@@ -429,6 +489,9 @@ tw_status tw_weave_run(tw_weave_t w, int64_t T, int64_t prefix_tokens, tw_weave_
                                  "scheduler.cpp:116-118");
   CUDA_TRY(cudaSetDevice(w->device));
   CUBLAS_TRY(cublasSetSmCountTarget(w->blas, mode == TW_MODE_WEAVE ? std::max(0, gemm_sm_target) : 0));
+  // TP mode: the fused op leaves the normed hidden in the comm OUTPUT; the
+  // unfused baseline normalises into a local buffer after the AllReduce.
+  w->X = (w->comm && mode != TW_MODE_UNFUSED) ? w->X_comm : w->X_local;
   cudaEvent_t ca = nullptr, cb = nullptr;
   // warm-up layer (cuBLAS heuristics, first-launch costs), not timed
   w->pool_used = 0;

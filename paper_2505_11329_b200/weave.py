@@ -101,6 +101,8 @@ def place_sequence_boundaries(lengths, total: int, prefix: int):
 def _weave_lib():
     lib = ctypes.CDLL(os.path.join(_LIBDIR, "libtw_weave.so"))
     lib.tw_weave_create.argtypes = [POINTER(LayerSpec), c_int64, c_int, POINTER(c_void_p)]
+    lib.tw_weave_create_tp.argtypes = [POINTER(LayerSpec), c_int64, c_void_p, POINTER(c_void_p)]
+    lib.tw_weave_create_tp.restype = c_int
     lib.tw_weave_destroy.argtypes = [c_void_p]
     lib.tw_weave_run.argtypes = [c_void_p, c_int64, c_int64, c_int, c_int, c_int, c_int, POINTER(c_float)]
     lib.tw_weave_trace.argtypes = [c_void_p, c_int, POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_int),
@@ -113,7 +115,10 @@ def _weave_lib():
 class LayerRunner:
     """One GPU's layer DAG on real streams (include/tw/tw_weave.h)."""
 
-    def __init__(self, model: str = "llama-70b", tp: int = 8, max_tokens: int = 8192, device: int = 0, **overrides):
+    def __init__(self, model: str = "llama-70b", tp: int = 8, max_tokens: int = 8192, device: int = 0,
+                 comm=None, **overrides):
+        """comm: a multi-process tw_comm_t (c_void_p) -> TP mode, the boundary
+        op is K1 over the communicator (tw_weave_create_tp)."""
         self._L = _weave_lib()
         cfg = dict(PRESETS[model])
         cfg.update(overrides)
@@ -121,7 +126,10 @@ class LayerRunner:
         self.spec = LayerSpec(tp=tp, **cfg)
         self.model = model
         h = c_void_p()
-        check(self._L.tw_weave_create(ctypes.byref(self.spec), max_tokens, device, ctypes.byref(h)))
+        if comm is not None:
+            check(self._L.tw_weave_create_tp(ctypes.byref(self.spec), max_tokens, comm, ctypes.byref(h)))
+        else:
+            check(self._L.tw_weave_create(ctypes.byref(self.spec), max_tokens, device, ctypes.byref(h)))
         self._h = h
 
     def close(self):

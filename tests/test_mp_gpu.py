@@ -71,6 +71,62 @@ WORKER = textwrap.dedent("""
 """)
 
 
+WEAVE_WORKER = textwrap.dedent("""
+    import ctypes, json, os, sys
+    sys.path.insert(0, {root!r})
+    import torch
+    import torch.distributed as dist
+    from paper_2505_11329_b200 import _lib, weave
+    from tools.bench_tp import rendezvous_id
+    dist.init_process_group("gloo")
+    rank, world = dist.get_rank(), dist.get_world_size()
+    torch.cuda.set_device(0)
+    T, H = 512, 1024
+    rid = rendezvous_id(dist)
+    h = ctypes.c_void_p()
+    _lib.check(_lib.lib.tw_comm_create_mp(world, rank, 0, T * H * 2, rid.encode(), _lib.TW_TRANSPORT_AUTO,
+                                          ctypes.byref(h)))
+    r = weave.LayerRunner("llama-70b", tp=world, max_tokens=T, comm=h, hidden=H, intermediate=2048, heads=16,
+                          kv_heads=4, head_dim=64)
+    out = {{}}
+    for mode, kw in (("fuseonly", {{}}), ("unfused", {{}}), ("tokenweave", {{"prefix": 320, "boundary_sms": 4}})):
+        dist.barrier()
+        out[mode] = r.run(T, mode, layers=2, **kw)
+        out[mode + "_ops"] = [(e["op"], e["split"], e["stream"]) for e in r.trace()]
+    _lib.check(_lib.lib.tw_comm_check(h))
+    print(json.dumps(out), flush=True)
+    dist.barrier()
+    r.close()
+    _lib.lib.tw_comm_destroy(h)
+    dist.destroy_process_group()
+""")
+
+
+def test_weave_tp_runner_two_processes(cuda, tmp_path):
+    """The TP weave runner (K1 boundary over a multi-process communicator):
+    every mode completes on both ranks with the reference's DAG shapes."""
+    world = 2
+    script = tmp_path / "ww.py"
+    script.write_text(WEAVE_WORKER.format(root=ROOT))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    procs = []
+    for rank in range(world):
+        env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                   WORLD_SIZE=str(world), TW_BARRIER_SPIN_LIMIT=str(1 << 28))
+        procs.append(subprocess.Popen([sys.executable, str(script)], env=env, stdout=subprocess.PIPE,
+                                      stderr=subprocess.STDOUT, text=True))
+    outs = [p.communicate(timeout=600)[0] for p in procs]
+    for p, o in zip(procs, outs):
+        assert p.returncode == 0, o
+    for o in outs:
+        res = json.loads([ln for ln in o.splitlines() if ln.startswith("{")][-1])
+        assert len(res["fuseonly_ops"]) == 4 and len(res["unfused_ops"]) == 4
+        ops = res["tokenweave_ops"]
+        assert len(ops) == 8 and sum(1 for op, _, st in ops if op == "fused_ar_norm" and st == "comm") == 4
+
+
 def test_two_processes_one_gpu_peer_fallback(cuda, orc, tmp_path):
     world, T, H = 2, 48, 1024
     script = tmp_path / "w.py"
