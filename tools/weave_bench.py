@@ -68,12 +68,63 @@ def bench_case(weave, r, T, layers, budgets, ref, model, tp):
     return row
 
 
+def main_tp(args, world):
+    """torchrun, one process per GPU: the weave with K1 (NVLS, else PEER) as the
+    boundary op at TP = world.  Every rank runs the same sequence; each number
+    is the max over ranks."""
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2505_11329_b200 import _lib, weave
+    from tools.bench_tp import max_over_ranks, rendezvous_id
+    rank = int(os.environ["RANK"])
+    ndev = torch.cuda.device_count()
+    local = int(os.environ.get("LOCAL_RANK", rank)) % max(ndev, 1)
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl" if ndev >= world else "gloo")
+    dev = "cuda" if ndev >= world else None
+    res = {"device": f"{world} ranks", "tp": world, "rows": []}
+    for model, tokens in (("llama-70b", [1024, 2048, 4096, 8192]), ("mixtral-8x22b", [4096, 8192])):
+        if args.quick:
+            tokens = tokens[-1:]
+        H = weave.PRESETS[model]["hidden"]
+        h = ctypes.c_void_p()
+        _lib.check(_lib.lib.tw_comm_create_mp(world, rank, local, max(tokens) * H * 2,
+                                              rendezvous_id(dist).encode(), _lib.TW_TRANSPORT_AUTO, ctypes.byref(h)))
+        r = weave.LayerRunner(model, tp=world, max_tokens=max(tokens), comm=h)
+        for T in tokens:
+            a, b, off, mode = weave.make_split_plan(T, threshold=r.threshold)
+            row = {"model": model, "T": T, "plan": {"prefix": a, "suffix": b, "mode": weave.SPLIT_MODES[mode]}}
+            for name, m, kw in (("unfused_us", "unfused", {}), ("fuseonly_us", "fuseonly", {}),
+                                ("nocomm_us", "nocomm", {})):
+                row[name] = max_over_ranks(r.run(T, m, layers=args.layers, **kw), dist, dev)
+            for sms in (8, 16):
+                for pname, pa in (("equal", T // 2), ("analytic", a)):
+                    if 0 < pa < T:
+                        row[f"weave_{pname}_sms{sms}_us"] = max_over_ranks(
+                            r.run(T, "tokenweave", prefix=pa, boundary_sms=sms, layers=args.layers), dist, dev)
+            if rank == 0:
+                res["rows"].append(row)
+                print(json.dumps(row), flush=True)
+        r.close()
+        _lib.lib.tw_comm_destroy(h)
+    if rank == 0 and args.out:
+        with open(args.out, "w") as f:
+            json.dump(res, f, indent=1)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--layers", type=int, default=6)
     ap.add_argument("--out", default="")
     ap.add_argument("--quick", action="store_true")
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        return main_tp(args, world)
     from paper_2505_11329_b200 import weave
     ref = None
     try:
