@@ -356,8 +356,11 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
     }
   }
   RowPlan plan;
-  if (!plan_rows(H, vec ? nv : 1, 256, &plan))
+  // <= 4 vectors per thread: two register sets (the software pipeline) stay spill-free
+  if (!plan_rows(H, vec ? nv : 1, H / (vec ? nv : 1) > 1024 ? 512 : 256, &plan))
     return fail(TW_ERR_DIMENSION, "rmsnorm_residual: hidden size too large for the row engine");
+  static const char* pipe_env = std::getenv("TW_ROWS_PIPELINE");
+  plan.pipeline = pipe_env && pipe_env[0] == '1';
   const int bpsm = std::max(1, rownorm_blocks_per_sm(plan, bf16, Xport::Local));
   const long long need = (T + plan.groups - 1) / plan.groups;
   const int grid = static_cast<int>(std::min<long long>(need, static_cast<long long>(sms) * bpsm));
@@ -606,10 +609,11 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
     return fail(TW_ERR_UNSUPPORTED, std::string(op) + ": NVLS transport needs H % " + std::to_string(nv) +
                                         " == 0 and 16-byte aligned buffers");
   RowPlan plan;
-  // NVLS: 128-thread row groups (4 rows in flight per CTA); PEER holds every
-  // rank's vector in registers before summing, so it uses wider groups
-  // (fewer vectors per thread) to stay spill-free.
-  if (!plan_rows(H, vec ? nv : 1, nvls ? 128 : 512, &plan))
+  // NVLS: 256-thread row groups, <= 4 vectors per thread so the software
+  // pipeline (next row's ld_reduce in flight) fits two register sets; PEER
+  // holds every rank's vector before summing, so it uses wider groups.
+  const long long nvec = H / (vec ? nv : 1);
+  if (!plan_rows(H, vec ? nv : 1, nvls ? (nvec > 1024 ? 512 : 256) : 512, &plan))
     return fail(TW_ERR_DIMENSION, std::string(op) + ": hidden size too large for the row engine");
   const Xport x = nvls ? Xport::Nvls : Xport::Peer;
 

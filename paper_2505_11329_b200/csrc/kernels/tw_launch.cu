@@ -46,33 +46,37 @@ namespace {
 
 using KernelFn = void (*)(RowParams);
 
-template <class E, int N, Xport X>
+template <class E, int N, Xport X, bool PF>
 KernelFn pick_rownorm(int vpt) {
   switch (vpt) {
-    case 1: return rownorm_kernel<E, N, 1, X>;
-    case 2: return rownorm_kernel<E, N, 2, X>;
-    case 4: return rownorm_kernel<E, N, 4, X>;
-    case 8: return rownorm_kernel<E, N, 8, X>;
-    case 16: return rownorm_kernel<E, N, 16, X>;
+    case 1: return rownorm_kernel<E, N, 1, X, PF>;
+    case 2: return rownorm_kernel<E, N, 2, X, PF>;
+    case 4: return rownorm_kernel<E, N, 4, X, PF>;
+    case 8: return rownorm_kernel<E, N, 8, X, PF>;
+    case 16: return rownorm_kernel<E, N, 16, X, PF>;
     default: return nullptr;
   }
 }
 
+// NVLS always runs the software-pipelined loop; PEER never (it already holds
+// every rank's vector); the local engine runs it on request (plan.pipeline).
 template <class E, int N>
-KernelFn pick_by_xport(Xport x, int vpt) {
+KernelFn pick_by_xport(Xport x, int vpt, bool pipeline) {
   switch (x) {
-    case Xport::Local: return pick_rownorm<E, N, Xport::Local>(vpt);
-    case Xport::Peer: return pick_rownorm<E, N, Xport::Peer>(vpt);
+    case Xport::Local:
+      return pipeline ? pick_rownorm<E, N, Xport::Local, true>(vpt) : pick_rownorm<E, N, Xport::Local, false>(vpt);
+    case Xport::Peer: return pick_rownorm<E, N, Xport::Peer, false>(vpt);
     case Xport::Nvls:
-      if constexpr (N > 1) return pick_rownorm<E, N, Xport::Nvls>(vpt);
+      if constexpr (N > 1) return pick_rownorm<E, N, Xport::Nvls, true>(vpt);
       return nullptr;
   }
   return nullptr;
 }
 
-KernelFn pick_kernel(bool bf16, int N, Xport x, int vpt) {
-  if (bf16) return N == 8 ? pick_by_xport<uint16_t, 8>(x, vpt) : pick_by_xport<uint16_t, 1>(x, vpt);
-  return N == 4 ? pick_by_xport<float, 4>(x, vpt) : pick_by_xport<float, 1>(x, vpt);
+KernelFn pick_kernel(bool bf16, int N, Xport x, int vpt, bool pipeline) {
+  if (bf16)
+    return N == 8 ? pick_by_xport<uint16_t, 8>(x, vpt, pipeline) : pick_by_xport<uint16_t, 1>(x, vpt, pipeline);
+  return N == 4 ? pick_by_xport<float, 4>(x, vpt, pipeline) : pick_by_xport<float, 1>(x, vpt, pipeline);
 }
 
 KernelFn pick_allreduce(bool bf16, int N, Xport x) {
@@ -101,6 +105,7 @@ bool plan_rows(long long H, int elems_per_vec, int tpr_pref, RowPlan* plan) {
       plan->vpt = vpt;
       plan->tpr = tpr;
       plan->groups = std::min(kMaxGroups, kBlock / tpr);
+      plan->pipeline = false;
       return true;
     }
   }
@@ -109,7 +114,7 @@ bool plan_rows(long long H, int elems_per_vec, int tpr_pref, RowPlan* plan) {
 
 cudaError_t launch_rownorm(const RowParams& params, const RowPlan& plan, bool bf16, Xport x, dim3 grid,
                            cudaStream_t stream) {
-  KernelFn fn = pick_kernel(bf16, plan.N, x, plan.vpt);
+  KernelFn fn = pick_kernel(bf16, plan.N, x, plan.vpt, plan.pipeline);
   if (!fn) return cudaErrorInvalidConfiguration;
   RowParams p = params;
   p.V = plan.V;
@@ -130,7 +135,7 @@ cudaError_t launch_allreduce(const RowParams& params, const RowPlan& plan, bool 
 }
 
 int rownorm_blocks_per_sm(const RowPlan& plan, bool bf16, Xport x) {
-  KernelFn fn = pick_kernel(bf16, plan.N, x, plan.vpt);
+  KernelFn fn = pick_kernel(bf16, plan.N, x, plan.vpt, plan.pipeline);
   if (!fn) return 0;
   int n = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reinterpret_cast<const void*>(fn), plan.groups * plan.tpr,

@@ -14,6 +14,7 @@ struct RowPlan {
   int vpt;     // vectors per thread
   int tpr;     // threads per row group
   int groups;  // row groups per CTA
+  bool pipeline;  // local engine: software-pipelined row loop (NVLS always pipelines)
 };
 
 // Chooses vectors-per-thread and threads-per-row for a row of H elements

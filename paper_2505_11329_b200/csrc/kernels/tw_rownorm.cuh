@@ -224,7 +224,12 @@ __device__ __forceinline__ void rank_barrier(const RowParams& p, const RankSlot&
 
 // ---- the row kernel ------------------------------------------------------------------
 
-template <class E, int N, int VPT, Xport X>
+// PF: software-pipelined row loop (next row's loads in flight during this
+// row's math and stores) -- the NVLS path, where ld_reduce latency is long;
+// the local (K2) engine defaults to PF=false, which measured faster for short
+// rows (TW_ROWS_PIPELINE=1 selects PF=true there, used by the tests to cover
+// the pipelined code on hardware).
+template <class E, int N, int VPT, Xport X, bool PF>
 __global__ void __launch_bounds__(kBlock, 1) rownorm_kernel(const __grid_constant__ RowParams p) {
   using VT = Vec<E, N>;
   using Raw = typename VT::Raw;
@@ -255,17 +260,14 @@ __global__ void __launch_bounds__(kBlock, 1) rownorm_kernel(const __grid_constan
     row1 = s.end;
   }
   const long long stride = static_cast<long long>(gridDim.x) * groups;
-  int parity = 0;
-  for (long long t = row0 + static_cast<long long>(blockIdx.x) * groups + group; t < row1;
-       t += stride, parity ^= 1) {
+  const void* res_src = (X == Xport::Local) ? p.res_in : s.residual;
+  void* res_dst = (X == Xport::Local) ? p.res_out : s.residual;
+  float xs[(X == Xport::Peer) ? VPT : 1][N];  // Peer: fp32 rank-sum accumulators
+
+  // Phase 1 of a row: issue every load of the row before using any of them.
+  auto load_row = [&](long long t, Raw (&xr)[VPT], Raw (&rr)[VPT]) {
     const long long rowe = (X == Xport::Local ? t : p.row_offset + t) * H;  // row in the [T,H] buffers
     const long long srow = (X == Xport::Local) ? rowe : (t - row0) * H;  // residual row
-    const void* res_src = (X == Xport::Local) ? p.res_in : s.residual;
-    void* res_dst = (X == Xport::Local) ? p.res_out : s.residual;
-
-    // Phase 1: issue every load of the row before using any of them.
-    Raw xr[VPT], rr[VPT];
-    float xs[(X == Xport::Peer) ? VPT : 1][N];  // Peer: fp32 rank-sum accumulators
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
       const int c = lt + k * tpr;
@@ -298,6 +300,12 @@ __global__ void __launch_bounds__(kBlock, 1) rownorm_kernel(const __grid_constan
         rr[k] = VT::load_stream(res_src, srow + static_cast<long long>(c) * N);
       }
     }
+  };
+
+  // Phases 2-4 of a row, once its loads are in registers.
+  auto finish_row = [&](long long t, Raw (&xr)[VPT], Raw (&rr)[VPT], int parity) {
+    const long long rowe = (X == Xport::Local ? t : p.row_offset + t) * H;
+    const long long srow = (X == Xport::Local) ? rowe : (t - row0) * H;
     // Phase 2: r' = x + res (fp32), rounded to the storage type and written
     // back; the sum of squares is taken over the stored (rounded) r' so the
     // output is exactly the RMSNorm of the residual the caller gets back.
@@ -364,6 +372,36 @@ __global__ void __launch_bounds__(kBlock, 1) rownorm_kernel(const __grid_constan
           for (int q = 0; q < p.world; ++q) VT::store(p.peer_out[q], rowe + e, ov);
         }
       }
+    }
+  };
+
+  const long long first = row0 + static_cast<long long>(blockIdx.x) * groups + group;
+  if constexpr (PF && X != Xport::Peer) {
+    // Software pipeline: the next row's loads are in flight while this row is
+    // reduced, normalised and stored (two register sets, ping-pong).
+    Raw xa[VPT], ra[VPT], xb[VPT], rb[VPT];
+    int parity = 0;
+    long long t = first;
+    if (t < row1) load_row(t, xa, ra);
+    while (t < row1) {
+      const long long tn = t + stride;
+      if (tn < row1) load_row(tn, xb, rb);
+      finish_row(t, xa, ra, parity);
+      parity ^= 1;
+      if (tn >= row1) break;
+      const long long tnn = tn + stride;
+      if (tnn < row1) load_row(tnn, xa, ra);
+      finish_row(tn, xb, rb, parity);
+      parity ^= 1;
+      t = tnn;
+    }
+  } else {
+    // Peer holds every rank's vector before the ordered sum: no second set.
+    int parity = 0;
+    for (long long t = first; t < row1; t += stride, parity ^= 1) {
+      Raw xr[VPT], rr[VPT];
+      load_row(t, xr, rr);
+      finish_row(t, xr, rr, parity);
     }
   }
 

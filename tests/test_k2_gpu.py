@@ -92,6 +92,22 @@ def test_k2_host_buffers_pipeline(cuda, orc, T, H, chunk, pinned):
     assert_bf16_close(out.float().numpy(), want_out)
 
 
+@pytest.mark.parametrize("engine,pipeline", [("rows", "1"), ("rows", "0"), ("bulk", "0"), ("tma", "0")])
+def test_k2_every_engine_matches_oracle(cuda, engine, pipeline):
+    """Every K2 engine (and the software-pipelined row loop that the NVLS K1
+    path uses) against the oracle: the parity tests above re-run in a
+    subprocess with the engine forced (the selection is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, TW_K2_ENGINE=engine, TW_ROWS_PIPELINE=pipeline)
+    p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
+                        "matches_oracle and not every_engine or in_place or full_size or host_buffers"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
+    assert " passed" in p.stdout
+
+
 def test_k2_zero_input_normalizes_to_zero(cuda):
     import torch
     import paper_2505_11329_b200 as tw
