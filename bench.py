@@ -344,7 +344,9 @@ def run_ours_single(args):
             sweep[str(t)] = {"us": round(us, 2), "hbm_gbs": round((4 * t * H * 2) / us / 1e3, 1)}
         line["tp1_sweep"] = sweep
         line["unfused_torch_add_rmsnorm_us"] = unfused_torch(T, H, flush)
-        line["k1_colocated_peer_us"] = {f"tp{n}": k1_colocated(T, H, n, 16, flush) for n in (2, 8)}
+        # simulated ranks share this GPU: the whole GPU split between them
+        line["k1_colocated_peer_us"] = {f"tp{n}_sms{148 // n}": k1_colocated(T, H, n, 148 // n, flush)
+                                        for n in (2, 8)}
         threads = os.cpu_count() or 1
         sample_T = 2048
         cpu_ms = reference_rmsnorm_ms(sample_T, H, threads, 3)
