@@ -344,8 +344,8 @@ def run_ours_single(args):
             sweep[str(t)] = {"us": round(us, 2), "hbm_gbs": round((4 * t * H * 2) / us / 1e3, 1)}
         line["tp1_sweep"] = sweep
         line["unfused_torch_add_rmsnorm_us"] = unfused_torch(T, H, flush)
-        # simulated ranks share this GPU: the whole GPU split between them
-        line["k1_colocated_peer_us"] = {f"tp{n}_sms{148 // n}": k1_colocated(T, H, n, 148 // n, flush)
+        # simulated ranks share this GPU: the whole GPU (2 CTAs/SM) split between them
+        line["k1_colocated_peer_us"] = {f"tp{n}_ctas{296 // n}": k1_colocated(T, H, n, 296 // n, flush)
                                         for n in (2, 8)}
         threads = os.cpu_count() or 1
         sample_T = 2048

@@ -230,7 +230,8 @@ __device__ __forceinline__ void rank_barrier(const RowParams& p, const RankSlot&
 // rows (TW_ROWS_PIPELINE=1 selects PF=true there, used by the tests to cover
 // the pipelined code on hardware).
 template <class E, int N, int VPT, Xport X, bool PF>
-__global__ void __launch_bounds__(kBlock, 1) rownorm_kernel(const __grid_constant__ RowParams p) {
+__global__ void __launch_bounds__(kBlock, (X == Xport::Peer && VPT <= 2) ? 2 : 1)
+    rownorm_kernel(const __grid_constant__ RowParams p) {
   using VT = Vec<E, N>;
   using Raw = typename VT::Raw;
   // fp32 activations keep the reference's double sum of squares.
@@ -279,21 +280,25 @@ __global__ void __launch_bounds__(kBlock, 1) rownorm_kernel(const __grid_constan
           xr[k] = VT::mm_reduce(p.mc_in, e);
         } else {
           // Rank-ascending fp32 sum from 0.0f (proj/src/collectives.cpp:74-78).
-          // All ranks' loads are issued before the first add (memory-level
-          // parallelism); the sum itself keeps the reference's order.
-          Raw raw[kMaxRanks];
-#pragma unroll
-          for (int q = 0; q < kMaxRanks; ++q)
-            if (q < p.world) raw[q] = VT::load(p.peer_in[q], e);
+          // Loads are issued four ranks at a time before their adds (memory-
+          // level parallelism within a register budget that allows two CTAs
+          // per SM); the sum itself keeps the reference's rank order.
 #pragma unroll
           for (int i = 0; i < N; ++i) xs[k][i] = 0.0f;
 #pragma unroll
-          for (int q = 0; q < kMaxRanks; ++q) {
-            if (q < p.world) {
-              float f[N];
-              VT::unpack(raw[q], f);
+          for (int h = 0; h < kMaxRanks; h += 4) {
+            Raw raw[4];
 #pragma unroll
-              for (int i = 0; i < N; ++i) xs[k][i] += f[i];
+            for (int q = 0; q < 4; ++q)
+              if (h + q < p.world) raw[q] = VT::load(p.peer_in[h + q], e);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (h + q < p.world) {
+                float f[N];
+                VT::unpack(raw[q], f);
+#pragma unroll
+                for (int i = 0; i < N; ++i) xs[k][i] += f[i];
+              }
             }
           }
         }
