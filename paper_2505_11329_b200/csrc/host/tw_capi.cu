@@ -325,9 +325,28 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
   const size_t rbytes = static_cast<size_t>(H) * (bf16 ? 2 : 4);
   bool want_rows = rbytes < 12 * 1024;
   bool tma_store = rbytes >= 16 * 1024;
+  // Under an explicit SM budget (the weave's boundary op) the flat engine moves
+  // the most bytes per SM (66 vs 48-57 GB/s/SM at 8-32 SMs, profiles/k2_engines_r01.txt).
+  bool want_flat = sm_budget > 0 && sm_budget <= 64;
   if (engine_env) {
     want_rows = std::strcmp(engine_env, "rows") == 0;
     tma_store = std::strcmp(engine_env, "tma") == 0;
+    want_flat = std::strcmp(engine_env, "flat") == 0;
+  }
+  if (vec && want_flat && H / nv <= 2048) {
+    FlatParams f = {};
+    f.in = input;
+    f.res_in = residual;
+    f.res_out = residual_out;
+    f.out = output;
+    f.weight = weight;
+    f.T = T;
+    f.H = H;
+    f.V = static_cast<int>(H / nv);
+    f.eps = eps;
+    cudaError_t e = launch_k2_flat(f, bf16, sms, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "rmsnorm_residual (flat) launch");
+    return TW_OK;
   }
   if (vec && !want_rows) {
     RowPlan bp;

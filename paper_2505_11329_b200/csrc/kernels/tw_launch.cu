@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "tw_bulk.cuh"
+#include "tw_flat.cuh"
 #include "tw_launch.h"
 #include "tw_rownorm.cuh"
 
@@ -176,6 +177,32 @@ cudaError_t launch_k2_bulk(const BulkParams& params, int vpt, bool bf16, int gri
   BulkParams p = params;
   void* args[] = {&p};
   return cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(params.tpr + 32), args, smem, stream);
+}
+
+// ---- K2 flat engine ----------------------------------------------------------------
+
+cudaError_t launch_k2_flat(const FlatParams& params, bool bf16, int sms, cudaStream_t stream) {
+  const int vpt_needed = (params.V + 1023) / 1024;
+  using FlatFn = void (*)(FlatParams);
+  FlatFn fn = nullptr;
+  int vpt = 0;
+  if (vpt_needed <= 1) {
+    fn = bf16 ? k2_flat_kernel<uint16_t, 1> : k2_flat_kernel<float, 1>;
+    vpt = 1;
+  } else if (vpt_needed <= 2) {
+    fn = bf16 ? k2_flat_kernel<uint16_t, 2> : k2_flat_kernel<float, 2>;
+    vpt = 2;
+  } else {
+    return cudaErrorInvalidConfiguration;
+  }
+  const int threads = std::max(32, ((params.V + vpt - 1) / vpt + 31) / 32 * 32);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn), threads, 0);
+  const long long grid = std::min<long long>(params.T, static_cast<long long>(sms) * std::max(per_sm, 1));
+  FlatParams p = params;
+  void* args[] = {&p};
+  return cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(static_cast<unsigned>(grid)), dim3(threads), args,
+                          0, stream);
 }
 
 // ---- finite scan (TokenMatrix::validate, numerics.cpp:25-27) ---------------------

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include "tw_bulk.cuh"
+#include "tw_flat.cuh"
 #include "tw_rownorm.cuh"
 
 namespace tw {
@@ -30,6 +31,8 @@ int rownorm_blocks_per_sm(const RowPlan& plan, bool bf16, Xport x);
 size_t bulk_smem_bytes(int stages, uint32_t row_bytes, int tpr);
 cudaError_t launch_k2_bulk(const BulkParams& params, int vpt, bool bf16, int grid, cudaStream_t stream,
                            bool tma_store);
+// K2 flat engine (tw_flat.cuh); V <= 2048 vectors per row.
+cudaError_t launch_k2_flat(const FlatParams& params, bool bf16, int sms, cudaStream_t stream);
 cudaError_t launch_count_nonfinite(const void* x, long long n, bool bf16, int* count, cudaStream_t stream);
 
 }  // namespace tw

@@ -43,6 +43,6 @@ if __name__ == "__main__":
         print(H_label(), run(H=int(sys.argv[2])))
     else:
         for H in (8192, 4096, 6144):
-            for eng in ("tma", "bulk", "rows"):
+            for eng in ("tma", "bulk", "rows", "flat"):
                 env = dict(os.environ, TW_K2_ENGINE=eng)
                 subprocess.run([sys.executable, __file__, "child", str(H)], env=env, check=True)

@@ -30,5 +30,5 @@ if __name__ == "__main__":
     if len(sys.argv) > 1:
         child()
     else:
-        for eng in ("tma", "bulk", "rows"):
+        for eng in ("tma", "bulk", "rows", "flat"):
             subprocess.run([sys.executable, __file__, "child"], env=dict(os.environ, TW_K2_ENGINE=eng), check=True)
