@@ -92,7 +92,7 @@ def test_k2_host_buffers_pipeline(cuda, orc, T, H, chunk, pinned):
     assert_bf16_close(out.float().numpy(), want_out)
 
 
-@pytest.mark.parametrize("engine,pipeline", [("rows", "1"), ("rows", "0"), ("bulk", "0"), ("tma", "0")])
+@pytest.mark.parametrize("engine,pipeline", [("rows", "1"), ("rows", "0"), ("bulk", "0"), ("tma", "0"), ("flat", "0")])
 def test_k2_every_engine_matches_oracle(cuda, engine, pipeline):
     """Every K2 engine (and the software-pipelined row loop that the NVLS K1
     path uses) against the oracle: the parity tests above re-run in a
@@ -153,9 +153,12 @@ def test_k2_sm_budget_does_not_change_results(cuda):
     r = torch.randn(300, 8192, device="cuda", dtype=torch.bfloat16)
     w = torch.rand(8192, device="cuda") + 0.5
     ref_out, ref_res = tw.rmsnorm_residual(x, r, w)
-    for budget in (1, 2, 8, 16, 148):
+    for budget in (1, 2, 8, 16, 64, 65, 148):
+        # budgets <= 64 select the flat engine: r' is bitwise identical, the
+        # output may differ by the row-sum order (one bf16 ulp at most)
         o, rr = tw.rmsnorm_residual(x, r, w, sm_budget=budget)
-        assert torch.equal(o, ref_out) and torch.equal(rr, ref_res)
+        assert torch.equal(rr, ref_res)
+        assert (o.float() - ref_out.float()).abs().max().item() <= 2 ** -7 * ref_out.float().abs().max().item()
 
 
 def test_k2_full_size_vs_torch_fp32_and_sampled_oracle(cuda, orc):
