@@ -325,9 +325,12 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
   const size_t rbytes = static_cast<size_t>(H) * (bf16 ? 2 : 4);
   bool want_rows = rbytes < 12 * 1024;
   bool tma_store = rbytes >= 16 * 1024;
-  // Under an explicit SM budget (the weave's boundary op) the flat engine moves
-  // the most bytes per SM (66 vs 48-57 GB/s/SM at 8-32 SMs, profiles/k2_engines_r01.txt).
-  bool want_flat = sm_budget > 0 && sm_budget <= 64;
+  // The flat engine moves the most bytes per SM when it runs alone under a
+  // budget (66 vs 48-57 GB/s/SM, profiles/k2_engines_r01.txt), but next to
+  // cuBLAS GEMMs (the weave) the TMA engine -- few threads, traffic issued by
+  // the bulk engine -- measured faster (1448 vs 1522 us per Llama layer), so
+  // flat is opt-in (TW_K2_ENGINE=flat).
+  bool want_flat = false;
   if (engine_env) {
     want_rows = std::strcmp(engine_env, "rows") == 0;
     tma_store = std::strcmp(engine_env, "tma") == 0;
