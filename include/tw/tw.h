@@ -6,7 +6,7 @@
  * arguments are cudaStream_t passed as void* (NULL = legacy default stream).
  *
  * Every entry point below replaces a reference interface (paths relative to
- * /root/reference); the drop-in C++ API (include/weavesim/*.hpp) is layered
+ * /root/reference); the drop-in C++ API (the include/weavesim headers) is layered
  * on top of these calls and keeps the reference signatures and exceptions.
  *
  * Threading: a communicator is not safe for concurrent mutation (the

@@ -74,6 +74,19 @@ def test_host_validation_before_any_device_work():
     assert b"epsilon" in L.tw_last_error()
 
 
+def test_c_abi_from_plain_c99(tmp_path):
+    """The headers are C (not C++) and the libraries link from gcc -std=c99."""
+    import subprocess
+    exe = tmp_path / "test_capi"
+    lib = os.path.join(ROOT, "paper_2505_11329_b200", "lib")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "c", "test_capi.c"), "-o", str(exe), "-L", lib, "-ltw",
+                    "-lweavesim_b200", "-ltw_weave", f"-Wl,-rpath,{lib}"], check=True)
+    p = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0, p.stdout + p.stderr
+    assert "c-abi: ok" in p.stdout
+
+
 def test_comm_requires_a_device_here():
     import paper_2505_11329_b200 as tw
     if tw.device_count() > 0:
