@@ -102,6 +102,42 @@ def run_tp(args):
     times = [s.elapsed_time(x) for s, x in zip(starts, ends)]
     us_local = 1e3 * sum(times) / len(times)
     us = max_over_ranks(us_local, dist, device=red_device)
+    # Unfused baselines on the same box (not timed in `value`): our one-shot
+    # AllReduce (K3) + K2 over the full T, and NCCL all_reduce + K2.
+    out_p = ctypes.c_void_p()
+    _lib.check(_lib.lib.tw_comm_buffer(h, rank, _lib.TW_BUF_OUTPUT, ctypes.byref(out_p)))
+    summed = torch.as_tensor(tw._DevBuf(out_p.value, (T * H,), "<i2"), device="cuda").view(torch.bfloat16).view(T, H)
+    full_res = torch.zeros(T, H, device="cuda", dtype=torch.bfloat16)
+    normed = torch.empty(T, H, device="cuda", dtype=torch.bfloat16)
+
+    def timed_baseline(fn, reps=10):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(reps):
+            fn()
+        e.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(1e3 * s.elapsed_time(e) / reps, dist, red_device)
+
+    def k3_k2():
+        _lib.check(_lib.lib.tw_allreduce(h, T, H, 0, _lib.TW_BF16, budget, stream.cuda_stream))
+        tw.rmsnorm_residual(summed, full_res, weight, residual_out=full_res, out=normed, stream=stream)
+
+    baselines = {"k3_allreduce_plus_k2_us": round(timed_baseline(k3_k2), 2)}
+    if red_device == "cuda":
+        nccl_buf = torch.zeros(T, H, device="cuda", dtype=torch.bfloat16)
+
+        def nccl_k2():
+            with torch.cuda.stream(stream):
+                dist.all_reduce(nccl_buf)
+            tw.rmsnorm_residual(nccl_buf, full_res, weight, residual_out=full_res, out=normed, stream=stream)
+
+        baselines["nccl_allreduce_plus_k2_us"] = round(timed_baseline(nccl_k2), 2)
+    _lib.check(_lib.lib.tw_comm_check(h))
     nvl = algorithmic_nvlink_bytes(T, H, world, gather)
     achieved = nvl / (us * 1e-6) / 1e9
     if rank == 0:
@@ -118,7 +154,7 @@ def run_tp(args):
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": 900.0, "unit": "GB/s",
                          "frac": round(achieved / 900.0, 4), "peak_kind": "nominal per direction",
                          "alg_bytes_per_launch": nvl, "traffic": None},
-            "gpu_launches": args.steps, "wall_s": round(wall, 3),
+            "gpu_launches": args.steps, "wall_s": round(wall, 3), "unfused_baselines": baselines,
         }
         print(json.dumps(line), flush=True)
     _lib.lib.tw_comm_destroy(h)
