@@ -62,8 +62,8 @@ def bench_case(weave, r, T, layers, budgets, ref, model, tp):
     lat = r.run(T, "tokenweave", prefix=best[1][0], boundary_sms=best[1][1],
                 gemm_sms=best[1][2] if len(best[1]) > 2 else 0, layers=layers)
     row["timeline"] = weave.timeline_json(r.trace(), lat)
-    if ref is not None and tp == 8:
-        row["reference_model_us"] = {m: 1e6 * ref.layer_latency("b200", model, T, m)
+    if (model, T) in ref and tp == 8:
+        row["reference_model_us"] = {m: 1e6 * ref[(model, T)][m]
                                      for m in ("multimem", "fuseonly", "tokenweave", "nocomm")}
     return row
 
@@ -126,12 +126,10 @@ def main():
     if world > 1:
         return main_tp(args, world)
     from paper_2505_11329_b200 import weave
-    ref = None
-    try:
-        import oracle  # reference simulator predictions ("predicted" column only)
-        ref = oracle.RefLib()
-    except Exception:
-        pass
+    # The reference simulator's predictions ("predicted" column), recorded in
+    # the golden fixtures by tests/golden/make_golden.py (no oracle import here).
+    with open(os.path.join(ROOT, "tests", "golden", "golden.json")) as f:
+        ref = {(r["model"], r["T"]): r for r in json.load(f)["layer_latency_s"]}
     cases = [("llama-70b", 1, [1024, 2048, 4096, 8192], (16, 32, 64)),
              ("llama-70b", 8, [1024, 2048, 4096, 8192], (16, 32, 64)),
              ("mixtral-8x22b", 8, [4096, 8192], (16, 32, 64))]
