@@ -110,7 +110,7 @@ struct DeviceGuard {
 
 static tw_status create_peer(tw_comm* c) {
   c->region = round_up(std::max<size_t>(c->bytes, 1), 256);
-  c->total = 3 * c->region + 4096;
+  c->total = 3 * c->region + kPadBytes;
   for (int r = 0; r < c->world; ++r) {
     RankBuffers& rb = c->ranks[r];
     cudaError_t e = cudaSetDevice(rb.device);
@@ -121,8 +121,9 @@ static tw_status create_peer(tw_comm* c) {
     rb.owns_cuda_malloc = true;
     for (int b = 0; b < 3; ++b) rb.buf[b] = base + b * c->region;
     rb.pad = reinterpret_cast<uint32_t*>(base + 3 * c->region);
-    rb.err = reinterpret_cast<int*>(base + 3 * c->region + 2048);
-    e = cudaMemset(base + 3 * c->region, 0, 4096);
+    rb.gen = reinterpret_cast<uint32_t*>(base + 3 * c->region + kPadGenOffset);
+    rb.err = reinterpret_cast<int*>(base + 3 * c->region + kPadErrOffset);
+    e = cudaMemset(base + 3 * c->region, 0, kPadBytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(pads)");
   }
   if (!c->colocated) {
@@ -207,8 +208,9 @@ static tw_status create_nvls(tw_comm* c) {
     }
     rb.pad = reinterpret_cast<uint32_t*>(uc + 3 * c->region);
     rb.mc_pad = reinterpret_cast<uint32_t*>(mcp + 3 * c->region);
-    rb.err = reinterpret_cast<int*>(uc + 3 * c->region + 2048);
-    cudaError_t e = cudaMemset(uc + 3 * c->region, 0, 4096);
+    rb.gen = reinterpret_cast<uint32_t*>(uc + 3 * c->region + kPadGenOffset);
+    rb.err = reinterpret_cast<int*>(uc + 3 * c->region + kPadErrOffset);
+    cudaError_t e = cudaMemset(uc + 3 * c->region, 0, kPadBytes);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemset(pads)");
   }
   for (RankBuffers& rb : c->ranks) {
@@ -652,7 +654,7 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
   } else {
     budget = std::min(budget, std::max(1, sms / (comm->colocated ? W : 1)));
   }
-  const uint32_t per_barrier = static_cast<uint32_t>(W) * static_cast<uint32_t>(budget);
+  budget = std::min(budget, kPadSlots);
   RowParams p = {};
   p.T = T;
   p.H = H;
@@ -660,8 +662,6 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
   p.eps = eps;
   p.flags = flags;
   p.world = W;
-  p.entry_target = static_cast<uint32_t>(comm->arrivals + per_barrier);
-  p.exit_target = static_cast<uint32_t>(comm->arrivals + 2ull * per_barrier);
   // Barrier poll bound (~2 s at the default) and the fault-injection hook of
   // the timeout path: TW_FAULT_DROP_ARRIVAL_RANK=r makes rank r never signal,
   // the B200 analogue of the reference's --inject-shard-fault
@@ -684,6 +684,7 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
     s.residual = fused ? residual_shards[r] : nullptr;
     s.weight = fused ? weights[r] : nullptr;
     s.pad = comm->ranks[r].pad;
+    s.gen = comm->ranks[r].gen;
   };
   auto launch = [&](const RowParams& pp, dim3 grid, cudaStream_t s) {
     return fused ? launch_rownorm(pp, plan, bf16, x, grid, s) : launch_allreduce(pp, plan, bf16, x, grid, s);
@@ -714,7 +715,6 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
       if (e != cudaSuccess) return cuda_fail(e, op);
     }
   }
-  comm->arrivals += 2ull * per_barrier;
   return TW_OK;
 }
 

@@ -48,7 +48,8 @@ const Driver& driver();
 struct RankBuffers {
   int device = 0;
   void* buf[3] = {nullptr, nullptr, nullptr};  // INPUT, OUTPUT, RESIDUAL (unicast)
-  uint32_t* pad = nullptr;                      // signal pad (unicast)
+  uint32_t* pad = nullptr;                      // signal counters (unicast)
+  uint32_t* gen = nullptr;                      // per-CTA-index launch generations
   int* err = nullptr;                           // barrier-timeout flag
   // NVLS
   void* mc_buf[3] = {nullptr, nullptr, nullptr};
@@ -70,7 +71,6 @@ struct tw_comm {
   bool colocated = false;   // every rank on the same device
   std::vector<tw::RankBuffers> ranks;
   CUmemGenericAllocationHandle mc = 0;
-  uint64_t arrivals = 0;    // cumulative signal-pad arrivals per rank (host mirror)
   int local_rank = -1;      // >= 0: multi-process communicator owning only this rank
 };
 

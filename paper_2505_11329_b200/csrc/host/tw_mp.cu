@@ -22,6 +22,7 @@
 #include <thread>
 #include <vector>
 
+#include "../kernels/tw_rownorm.cuh"
 #include "tw_internal.h"
 
 namespace tw {
@@ -278,8 +279,9 @@ tw_status create_nvls_mp(tw_comm* c, int rank, const char* id) {
   }
   rb.pad = reinterpret_cast<uint32_t*>(uc + 3 * c->region);
   rb.mc_pad = reinterpret_cast<uint32_t*>(mcp + 3 * c->region);
-  rb.err = reinterpret_cast<int*>(uc + 3 * c->region + 2048);
-  cudaError_t e = cudaMemset(uc + 3 * c->region, 0, 4096);
+  rb.gen = reinterpret_cast<uint32_t*>(uc + 3 * c->region + kPadGenOffset);
+  rb.err = reinterpret_cast<int*>(uc + 3 * c->region + kPadErrOffset);
+  cudaError_t e = cudaMemset(uc + 3 * c->region, 0, kPadBytes);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cuda_fail(e, "zero signal pad");
   if (!rv.barrier(&err)) return fail(TW_ERR_CONFIG, err);  // every pad zeroed before any signal
@@ -291,15 +293,16 @@ tw_status create_nvls_mp(tw_comm* c, int rank, const char* id) {
 tw_status create_peer_mp(tw_comm* c, int rank, const std::string& id) {
   RankBuffers& rb = c->ranks[rank];
   c->region = round_up(std::max<size_t>(c->bytes, 1), 256);
-  c->total = 3 * c->region + 4096;
+  c->total = 3 * c->region + kPadBytes;
   char* base = nullptr;
   cudaError_t e = cudaMalloc(&base, c->total);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(comm buffers)");
   rb.owns_cuda_malloc = true;
   for (int b = 0; b < 3; ++b) rb.buf[b] = base + b * c->region;
   rb.pad = reinterpret_cast<uint32_t*>(base + 3 * c->region);
-  rb.err = reinterpret_cast<int*>(base + 3 * c->region + 2048);
-  e = cudaMemset(base + 3 * c->region, 0, 4096);
+  rb.gen = reinterpret_cast<uint32_t*>(base + 3 * c->region + kPadGenOffset);
+  rb.err = reinterpret_cast<int*>(base + 3 * c->region + kPadErrOffset);
+  e = cudaMemset(base + 3 * c->region, 0, kPadBytes);
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return cuda_fail(e, "zero signal pad");
   cudaIpcMemHandle_t mine;
@@ -320,7 +323,8 @@ tw_status create_peer_mp(tw_comm* c, int rank, const std::string& id) {
     char* pbase = static_cast<char*>(peer);
     for (int b = 0; b < 3; ++b) pb.buf[b] = pbase + b * c->region;
     pb.pad = reinterpret_cast<uint32_t*>(pbase + 3 * c->region);
-    pb.err = reinterpret_cast<int*>(pbase + 3 * c->region + 2048);
+    pb.gen = reinterpret_cast<uint32_t*>(pbase + 3 * c->region + kPadGenOffset);
+    pb.err = reinterpret_cast<int*>(pbase + 3 * c->region + kPadErrOffset);
   }
   if (!rv.barrier(&err)) return fail(TW_ERR_CONFIG, err);  // every pad zeroed and mapped before any signal
   return TW_OK;

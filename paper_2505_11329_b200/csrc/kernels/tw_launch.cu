@@ -18,7 +18,7 @@ template <class E, int N, Xport X>
 __global__ void __launch_bounds__(kBlock, 1) allreduce_kernel(const __grid_constant__ RowParams p) {
   using VT = Vec<E, N>;
   const RankSlot& s = p.slot[blockIdx.y];
-  rank_barrier<X>(p, s, p.entry_target);
+  rank_barrier<X>(p, s, 1);
   const long long n = (s.end - s.begin) * p.V;  // vectors in the shard
   const long long base = (p.row_offset + s.begin) * p.H;
   for (long long v = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kBlock, 1) allreduce_kernel(const __grid_const
       for (int q = 0; q < p.world; ++q) VT::store(p.peer_out[q], e, packed);
     }
   }
-  rank_barrier<X>(p, s, p.exit_target);
+  rank_barrier<X>(p, s, 2);
 }
 
 namespace {

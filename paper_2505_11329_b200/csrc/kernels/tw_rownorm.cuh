@@ -14,9 +14,10 @@
 // one named barrier per row (no __syncthreads on the row path).
 //
 // K1 brackets the row loop with the cross-rank signal-pad barrier
-// (PAPER.md:418,453): every CTA of every rank adds 1 to every rank's pad
-// (multimem.red on NVLS, red.release per peer otherwise) and waits on its own
-// pad with ld.acquire.sys for the host-tracked cumulative target.
+// (PAPER.md:418,453): CTA b of every rank adds 1 to counter b of every rank's
+// pad (multimem.red on NVLS, red per peer otherwise) and waits on its own
+// counter b with ld.acquire.sys for a target derived from CTA b's launch
+// generation, kept in device memory (graph-replayable, no host epoch).
 #pragma once
 
 #include <cstdint>
@@ -38,8 +39,18 @@ struct RankSlot {
   long long begin, end;  // owned token shard [begin, end)
   void* residual;        // shard rows [end-begin, H], updated in place
   const float* weight;   // fp32[H] on this device
-  uint32_t* pad;         // this rank's own signal pad (unicast VA)
+  uint32_t* pad;         // this rank's signal counters, one per CTA index (unicast VA)
+  uint32_t* gen;         // this rank's per-CTA-index launch generations (device-resident)
 };
+
+// Signal-pad granule of one rank: arrival counters for up to kPadSlots CTA
+// indices, then each CTA index's launch generation, then the timeout flag.
+// Barriers need no host-side epoch, so launches can be captured in CUDA
+// graphs and replayed.
+constexpr int kPadSlots = 1024;
+constexpr size_t kPadGenOffset = 4096;
+constexpr size_t kPadErrOffset = 8192;
+constexpr size_t kPadBytes = 16384;
 
 struct RowParams {
   long long T, H;
@@ -66,7 +77,6 @@ struct RowParams {
   void* mc_out;
   void* mc_res;
   uint32_t* mc_pad;
-  uint32_t entry_target, exit_target;
   int* err;
   long long spin_limit;   // barrier poll bound before the timeout flag is raised
   int drop_arrival_rank;  // fault injection (tests): this rank never signals; -1 = none
@@ -196,21 +206,29 @@ __device__ __forceinline__ Acc warp_sum(Acc v) {
 // ---- cross-rank barrier ------------------------------------------------------------
 
 template <Xport X>
-__device__ __forceinline__ void rank_barrier(const RowParams& p, const RankSlot& s, uint32_t target) {
+// phase 1 = entry, 2 = exit.  CTA b's g-th launch waits for its counter to
+// reach world*(2g+phase); the exit barrier then advances the CTA's generation
+// (only CTA b of this rank writes gen[b]; the next launch reads it after the
+// kernel boundary).  Every rank launches the same CTA count per call, so the
+// counters of CTA index b advance in lockstep across ranks.
+__device__ __forceinline__ void rank_barrier(const RowParams& p, const RankSlot& s, int phase) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    const int b = blockIdx.x;  // per-block-index counters: CTA b meets CTA b of every rank
+    const uint32_t g = *reinterpret_cast<volatile uint32_t*>(s.gen + b);
+    const uint32_t target = static_cast<uint32_t>(p.world) * (2u * g + static_cast<uint32_t>(phase));
     // The CTA's prior writes are ordered before the arrival by bar.sync
     // (cumulativity) + release semantics at system scope.
     if (s.rank != p.drop_arrival_rank) {  // fault injection: a rank that never arrives
       if constexpr (X == Xport::Nvls) {
-        mm_red_release_add(p.mc_pad, 1u);  // one op reaches every rank's pad
+        mm_red_release_add(p.mc_pad + b, 1u);  // one op reaches every rank's pad
       } else {
         fence_acq_rel_sys();
-        for (int q = 0; q < p.world; ++q) red_relaxed_add(p.peer_pad[q], 1u);
+        for (int q = 0; q < p.world; ++q) red_relaxed_add(p.peer_pad[q] + b, 1u);
       }
     }
     long long spins = 0;
-    while (static_cast<int>(ld_acquire(s.pad) - target) < 0) {
+    while (static_cast<int>(ld_acquire(s.pad + b) - target) < 0) {
       if (++spins > p.spin_limit) {  // bounded: a rank was never launched / died
         atomicExch(p.err, 1);
         break;
@@ -218,6 +236,7 @@ __device__ __forceinline__ void rank_barrier(const RowParams& p, const RankSlot&
       __nanosleep(64);
     }
     if constexpr (X == Xport::Nvls) fence_proxy_alias();
+    if (phase == 2) s.gen[b] = g + 1u;
   }
   __syncthreads();
 }
@@ -249,7 +268,7 @@ __global__ void __launch_bounds__(kBlock, (X == Xport::Peer && VPT <= 2) ? 2 : 1
   const long long H = p.H;
 
   if constexpr (X != Xport::Local) {
-    rank_barrier<X>(p, s, p.entry_target);
+    rank_barrier<X>(p, s, 1);
   }
 
   long long row0, row1;
@@ -410,7 +429,7 @@ __global__ void __launch_bounds__(kBlock, (X == Xport::Peer && VPT <= 2) ? 2 : 1
     }
   }
 
-  if constexpr (X != Xport::Local) rank_barrier<X>(p, s, p.exit_target);
+  if constexpr (X != Xport::Local) rank_barrier<X>(p, s, 2);
 }
 
 }  // namespace tw
