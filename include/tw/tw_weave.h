@@ -71,6 +71,14 @@ TW_API tw_status tw_weave_destroy(tw_weave_t w);
 TW_API tw_status tw_weave_run(tw_weave_t w, int64_t T, int64_t prefix_tokens, tw_weave_mode mode,
                               int boundary_sm_budget, int gemm_sm_target, int layers, float* us_per_layer);
 
+/* tw_weave_run with flags: TW_WEAVE_CUDA_GRAPH captures the `layers` chained
+ * layers (both streams, every DAG edge) into one CUDA graph, replays it and
+ * times the replay -- no per-launch host cost.  No per-op trace is recorded. */
+#define TW_WEAVE_CUDA_GRAPH 0x1u
+TW_API tw_status tw_weave_run_ex(tw_weave_t w, int64_t T, int64_t prefix_tokens, tw_weave_mode mode,
+                                 int boundary_sm_budget, int gemm_sm_target, int layers, unsigned flags,
+                                 float* us_per_layer);
+
 /* Per-event timestamps (us from the run's start) of the LAST layer of the
  * last tw_weave_run: op (tw_weave_op), split (0 prefix, 1 suffix, 2 whole),
  * stream (0 compute, 1 boundary).  Arrays hold max_events entries. */

@@ -68,6 +68,7 @@ struct tw_weave {
   std::vector<Ev> pool;
   size_t pool_used = 0;
   std::vector<size_t> last_layer_events;
+  bool tracing = true;  // per-op timing events (off while capturing a CUDA graph)
   cudaEvent_t t0 = nullptr;
   std::vector<cudaEvent_t> dag;  // edge events
   size_t dag_used = 0;
@@ -105,6 +106,7 @@ cudaEvent_t edge(tw_weave* w) {
 }
 
 size_t op_begin(tw_weave* w, int op, int split, int stream_id, cudaStream_t s) {
+  if (!w->tracing) return 0;  // CUDA-graph capture: no per-op timing events
   if (w->pool_used == w->pool.size()) {
     Ev e{};
     cudaEventCreate(&e.start);
@@ -119,7 +121,9 @@ size_t op_begin(tw_weave* w, int op, int split, int stream_id, cudaStream_t s) {
   return w->pool_used++;
 }
 
-void op_end(tw_weave* w, size_t id, cudaStream_t s) { cudaEventRecord(w->pool[id].end, s); }
+void op_end(tw_weave* w, size_t id, cudaStream_t s) {
+  if (w->tracing) cudaEventRecord(w->pool[id].end, s);
+}
 
 // ---- layer ops -------------------------------------------------------------------
 
@@ -477,11 +481,86 @@ tw_status layer(tw_weave* w, int64_t T, int64_t ta, tw_weave_mode mode, int budg
 
 }  // namespace
 
+namespace {
+
+// `layers` chained layers captured once into a CUDA graph (both streams:
+// the boundary stream joins the capture through the DAG's events) and replayed;
+// the replay is timed.  Removes the per-launch CPU cost of the ~15 launches
+// and event edges per layer.  Valid in TP mode too: the fused op's barrier
+// state lives in device memory, so a replayed launch is a fresh launch.
+tw_status run_graph(tw_weave* w, int64_t T, int64_t prefix, tw_weave_mode mode, int budget, int gemm_sms,
+                    int layers, float* us_per_layer) {
+  if (T < 1 || T > w->max_tokens) return werr(TW_ERR_DIMENSION, "weave_run: T out of range");
+  if (layers < 1) return werr(TW_ERR_CONFIG, "weave_run: layers must be >= 1");
+  if (mode == TW_MODE_WEAVE && (prefix < 1 || prefix >= T))
+    return werr(TW_ERR_CONTRACT, "weave_run: TokenWeave requires an Overlap split (0 < prefix < T)");
+  CUDA_TRY(cudaSetDevice(w->device));
+  CUBLAS_TRY(cublasSetSmCountTarget(w->blas, mode == TW_MODE_WEAVE ? std::max(0, gemm_sms) : 0));
+  w->X = (w->comm && mode != TW_MODE_UNFUSED) ? w->X_comm : w->X_local;
+  cudaEvent_t ca = nullptr, cb = nullptr;
+  w->tracing = false;
+  w->dag_used = 0;
+  tw_status st = layer(w, T, prefix, mode, budget, ca, cb);  // eager warm-up (cuBLAS setup)
+  if (st == TW_OK) {
+    cudaError_t e = cudaStreamSynchronize(w->compute);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(w->boundary);
+    if (e != cudaSuccess) st = werr(TW_ERR_CUDA, std::string("weave graph warm-up: ") + cudaGetErrorString(e));
+  }
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  if (st == TW_OK) {
+    w->dag_used = 0;
+    ca = cb = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(w->compute, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) st = werr(TW_ERR_CUDA, std::string("begin capture: ") + cudaGetErrorString(e));
+    for (int l = 0; st == TW_OK && l < layers; ++l) st = layer(w, T, prefix, mode, budget, ca, cb);
+    if (st == TW_OK) {
+      if (cb) cudaStreamWaitEvent(w->compute, cb, 0);
+      if (ca) cudaStreamWaitEvent(w->compute, ca, 0);
+    }
+    e = cudaStreamEndCapture(w->compute, &graph);
+    if (st == TW_OK && e != cudaSuccess) st = werr(TW_ERR_CUDA, std::string("end capture: ") + cudaGetErrorString(e));
+    if (st == TW_OK) {
+      e = cudaGraphInstantiate(&exec, graph, 0);
+      if (e != cudaSuccess) st = werr(TW_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+    }
+  }
+  if (st == TW_OK) {
+    cudaEvent_t t1 = nullptr;
+    cudaError_t e = cudaGraphLaunch(exec, w->compute);  // warm replay
+    if (e == cudaSuccess) e = cudaEventCreate(&t1);
+    if (e == cudaSuccess) e = cudaEventRecord(w->t0, w->compute);
+    if (e == cudaSuccess) e = cudaGraphLaunch(exec, w->compute);
+    if (e == cudaSuccess) e = cudaEventRecord(t1, w->compute);
+    if (e == cudaSuccess) e = cudaEventSynchronize(t1);
+    float ms = 0;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, w->t0, t1);
+    if (t1) cudaEventDestroy(t1);
+    if (e != cudaSuccess) st = werr(TW_ERR_CUDA, std::string("graph replay: ") + cudaGetErrorString(e));
+    *us_per_layer = 1000.0f * ms / layers;
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  w->tracing = true;
+  w->last_layer_events.clear();
+  cublasSetSmCountTarget(w->blas, 0);
+  return st;
+}
+
+}  // namespace
+
 extern "C" {
 
 tw_status tw_weave_run(tw_weave_t w, int64_t T, int64_t prefix_tokens, tw_weave_mode mode, int boundary_sm_budget,
                        int gemm_sm_target, int layers, float* us_per_layer) {
+  return tw_weave_run_ex(w, T, prefix_tokens, mode, boundary_sm_budget, gemm_sm_target, layers, 0u, us_per_layer);
+}
+
+tw_status tw_weave_run_ex(tw_weave_t w, int64_t T, int64_t prefix_tokens, tw_weave_mode mode, int boundary_sm_budget,
+                          int gemm_sm_target, int layers, unsigned flags, float* us_per_layer) {
   if (!w || !us_per_layer) return werr(TW_ERR_CONFIG, "weave_run: null argument");
+  if (flags & TW_WEAVE_CUDA_GRAPH) return run_graph(w, T, prefix_tokens, mode, boundary_sm_budget, gemm_sm_target,
+                                                    layers, us_per_layer);
   if (T < 1 || T > w->max_tokens) return werr(TW_ERR_DIMENSION, "weave_run: T out of range");
   if (layers < 1) return werr(TW_ERR_CONFIG, "weave_run: layers must be >= 1");
   if (mode == TW_MODE_WEAVE && (prefix_tokens < 1 || prefix_tokens >= T))

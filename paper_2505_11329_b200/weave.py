@@ -105,6 +105,9 @@ def _weave_lib():
     lib.tw_weave_create_tp.restype = c_int
     lib.tw_weave_destroy.argtypes = [c_void_p]
     lib.tw_weave_run.argtypes = [c_void_p, c_int64, c_int64, c_int, c_int, c_int, c_int, POINTER(c_float)]
+    lib.tw_weave_run_ex.argtypes = [c_void_p, c_int64, c_int64, c_int, c_int, c_int, c_int, ctypes.c_uint,
+                                    POINTER(c_float)]
+    lib.tw_weave_run_ex.restype = c_int
     lib.tw_weave_trace.argtypes = [c_void_p, c_int, POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_int),
                                    POINTER(c_float), POINTER(c_float)]
     for f in ("tw_weave_create", "tw_weave_destroy", "tw_weave_run", "tw_weave_trace"):
@@ -144,10 +147,12 @@ class LayerRunner:
             pass
 
     def run(self, T: int, mode: str, prefix: int = 0, boundary_sms: int = 16, gemm_sms: int = 0,
-            layers: int = 4) -> float:
+            layers: int = 4, graph: bool = False) -> float:
+        """Device time per layer (us).  graph=True: the layers are captured in
+        one CUDA graph and the replay is timed (no per-op trace)."""
         us = c_float()
-        check(self._L.tw_weave_run(self._h, T, prefix, MODES[mode], boundary_sms, gemm_sms, layers,
-                                   ctypes.byref(us)))
+        check(self._L.tw_weave_run_ex(self._h, T, prefix, MODES[mode], boundary_sms, gemm_sms, layers,
+                                      1 if graph else 0, ctypes.byref(us)))
         return us.value
 
     def trace(self, max_events: int = 64):

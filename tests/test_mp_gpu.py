@@ -93,6 +93,9 @@ WEAVE_WORKER = textwrap.dedent("""
         dist.barrier()
         out[mode] = r.run(T, mode, layers=2, **kw)
         out[mode + "_ops"] = [(e["op"], e["split"], e["stream"]) for e in r.trace()]
+    dist.barrier()
+    # K1 inside a CUDA graph, replayed: barrier generations live on the device
+    out["tokenweave_graph"] = r.run(T, "tokenweave", prefix=320, boundary_sms=4, layers=2, graph=True)
     _lib.check(_lib.lib.tw_comm_check(h))
     print(json.dumps(out), flush=True)
     dist.barrier()

@@ -76,6 +76,22 @@ def test_layer_runner_modes_and_dag(cuda, model):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["fuseonly", "tokenweave", "unfused", "nocomm"])
+def test_layer_runner_cuda_graph(cuda, mode):
+    """Capturing the chained layers in one CUDA graph: every mode replays, and
+    the replay is not slower than eager launches (it removes host cost)."""
+    from paper_2505_11329_b200 import weave
+    T = 1024
+    r = weave.LayerRunner("llama-70b", tp=8, max_tokens=T)
+    kw = {"prefix": T // 2, "boundary_sms": 32} if mode == "tokenweave" else {}
+    eager = min(r.run(T, mode, layers=4, **kw) for _ in range(2))
+    graph = min(r.run(T, mode, layers=4, graph=True, **kw) for _ in range(2))
+    assert 0 < graph <= eager * 1.10, (eager, graph)
+    assert len(r.trace()) == 0  # graph runs record no per-op trace
+    r.close()
+
+
+@pytest.mark.gpu
 def test_weave_contract_errors(cuda):
     import paper_2505_11329_b200 as tw
     from paper_2505_11329_b200 import weave
