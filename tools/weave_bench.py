@@ -59,6 +59,13 @@ def bench_case(weave, r, T, layers, budgets, ref, model, tp):
                                 "gemm_sms": best[1][2] if len(best[1]) > 2 else 0}
     row["speedup_vs_unfused"] = row["unfused_us"] / best[0]
     row["speedup_vs_fuseonly"] = row["fuseonly_us"] / best[0]
+    # the same layers captured in one CUDA graph (no per-launch host cost)
+    row["graph_us"] = {
+        "unfused": r.run(T, "unfused", layers=layers, graph=True),
+        "fuseonly": r.run(T, "fuseonly", layers=layers, graph=True),
+        "tokenweave": r.run(T, "tokenweave", prefix=best[1][0], boundary_sms=best[1][1],
+                            gemm_sms=best[1][2] if len(best[1]) > 2 else 0, layers=layers, graph=True),
+    }
     lat = r.run(T, "tokenweave", prefix=best[1][0], boundary_sms=best[1][1],
                 gemm_sms=best[1][2] if len(best[1]) > 2 else 0, layers=layers)
     row["timeline"] = weave.timeline_json(r.trace(), lat)
