@@ -172,6 +172,37 @@ def test_k1_repeated_launches_and_budgets(cuda, orc):
     comm.close()
 
 
+def test_k1_known_answers(cuda):
+    """N=2, T=2, H=2, inputs all ones, residual 0, w 1, eps 0 ->
+    out 1.0, residual 2.0; SPEC.md:104-105 -- AllReduce of N=4 ones -> 4 and of
+    rank-constant r -> 6 (K3)."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    for dt in (torch.float32, torch.bfloat16):
+        comm = tw.Communicator(2, [0, 0], 64, tw.TW_TRANSPORT_PEER)
+        for q in range(2):
+            comm.buffer(q, 0, (2, 2), dt).fill_(1.0)
+        shards = [torch.zeros(1, 2, device="cuda", dtype=dt) for _ in range(2)]
+        comm.fused_allreduce_rmsnorm(2, 2, shards, [torch.ones(2, device="cuda")] * 2, eps=0.0, dtype=dt)
+        torch.cuda.synchronize()
+        for q in range(2):
+            assert torch.all(comm.buffer(q, 1, (2, 2), dt) == 1.0)
+            assert torch.all(shards[q] == 2.0)
+        comm.close()
+        comm = tw.Communicator(4, [0] * 4, 3 * 8 * 4, tw.TW_TRANSPORT_PEER)
+        for q in range(4):
+            comm.buffer(q, 0, (3, 8), dt).fill_(1.0)
+        comm.allreduce(3, 8, dt)
+        torch.cuda.synchronize()
+        assert all(torch.all(comm.buffer(q, 1, (3, 8), dt) == 4.0) for q in range(4))
+        for q in range(4):
+            comm.buffer(q, 0, (3, 8), dt).fill_(float(q))
+        comm.allreduce(3, 8, dt)
+        torch.cuda.synchronize()
+        assert all(torch.all(comm.buffer(q, 1, (3, 8), dt) == 6.0) for q in range(4))
+        comm.close()
+
+
 def test_k1_barrier_timeout_fault_injection(cuda, monkeypatch):
     """A rank that never arrives must not hang the GPU: the bounded spin raises
     the timeout flag and tw_comm_check reports BarrierTimeout."""

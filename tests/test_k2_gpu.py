@@ -108,6 +108,17 @@ def test_k2_every_engine_matches_oracle(cuda, engine, pipeline):
     assert " passed" in p.stdout
 
 
+def test_k2_known_answer_single_token(cuda):
+    """T=1, H=1: in 3, res 1, w 2, eps 0 -> out 2, res 4 (exact)."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    for dt in (torch.float32, torch.bfloat16):
+        x = torch.tensor([[3.0]], device="cuda", dtype=dt)
+        r = torch.tensor([[1.0]], device="cuda", dtype=dt)
+        out, rout = tw.rmsnorm_residual(x, r, torch.tensor([2.0], device="cuda"), eps=0.0)
+        assert out.item() == 2.0 and rout.item() == 4.0
+
+
 def test_k2_zero_input_normalizes_to_zero(cuda):
     import torch
     import paper_2505_11329_b200 as tw
