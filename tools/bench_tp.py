@@ -75,6 +75,10 @@ def run_tp(args):
     weight = torch.rand(H, device="cuda", generator=g) + 0.5
     stream = torch.cuda.Stream()
     budget = int(getattr(args, "sm_budget", 16))
+    if transport == "peer":
+        # the P2P fallback hides NVLink load latency with more CTAs in flight
+        # (no in-switch reduction: every rank's vector crosses the link)
+        budget = max(budget, 48)
     flags = _lib.TW_GATHER_RESIDUAL if gather else 0
 
     def step():
