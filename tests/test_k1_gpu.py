@@ -172,6 +172,28 @@ def test_k1_repeated_launches_and_budgets(cuda, orc):
     comm.close()
 
 
+@pytest.mark.parametrize("dtype_name", ["float32", "bfloat16"])
+def test_k1_baseline_config0(cuda, orc, dtype_name):
+    """BASELINE.json configs[0]: 2 ranks, 1024 tokens x 4096 hidden, vs the
+    oracle on the same inputs (the reference's CPU-runnable case)."""
+    import torch
+    dtype = getattr(torch, dtype_name)
+    W, T, H = 2, 1024, 4096
+    inputs, residual, weight = group_inputs(2505, W, T, H)
+    import paper_2505_11329_b200 as tw
+    ranges = tw.token_shard_map(T, W)
+    inputs, residual, want_out, want_res = oracle_case(orc, inputs, residual, weight, ranges,
+                                                       dtype == torch.bfloat16)
+    outs, res, _ = run_k1(inputs, residual, weight, dtype, sm_budget=16)
+    for r in range(W):
+        if dtype == torch.float32:
+            assert_abs_close(outs[r], want_out, 1e-5)
+            assert np.array_equal(res[r], want_res[r])
+        else:
+            assert_bf16_close(outs[r], want_out)
+            assert np.array_equal(res[r], bf16_round(want_res[r]))
+
+
 def test_k1_known_answers(cuda):
     """N=2, T=2, H=2, inputs all ones, residual 0, w 1, eps 0 ->
     out 1.0, residual 2.0; SPEC.md:104-105 -- AllReduce of N=4 ones -> 4 and of
