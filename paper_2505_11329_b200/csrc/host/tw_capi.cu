@@ -360,9 +360,12 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
     // groups per SM double the per-SM rate of the pipeline (16.4 vs 18.5 us
     // at T=1024, 84.4 vs 85.4 us at 8192; H=6144: 65.6 vs 74 us; tools/k2_cps.py).
     static const char* cps_env = std::getenv("TW_K2_CTAS_PER_SM");
-    const int cps = cps_env ? std::max(1, std::min(4, std::atoi(cps_env))) : 2;
-    const size_t smem_budget = 200 * 1024 / cps;
-    const int stages = static_cast<int>(std::min<size_t>(8, smem_budget / (2ull * row_bytes)));
+    int cps = cps_env ? std::max(1, std::min(4, std::atoi(cps_env))) : 2;
+    int stages = static_cast<int>(std::min<size_t>(8, (200 * 1024 / cps) / (2ull * row_bytes)));
+    if (stages < 2 && cps > 1) {  // long rows (>= 25 KB): one CTA per SM keeps a 2+ stage ring
+      cps = 1;
+      stages = static_cast<int>(std::min<size_t>(8, (200 * 1024) / (2ull * row_bytes)));
+    }
     if (plan_rows(H, nv, H / nv > 1024 ? 512 : 256, &bp) && bp.vpt <= 8 && bp.tpr <= kBulkMaxConsumers &&
         stages >= 2) {
       BulkParams q = {};
