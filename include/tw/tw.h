@@ -84,8 +84,8 @@ TW_API int tw_device_count(void);
  *   residual_out = input + residual;  output = residual_out * rsqrt(mean(residual_out^2)+eps) * weight
  * input/residual/residual_out/output are [T,H] row-major of `dtype`; weight is
  * fp32[H].  residual_out may alias residual (in-place update); no other
- * aliasing.  sm_budget <= 0 means "whole GPU"; > 0 caps the CTAs launched
- * (two co-reside per SM on the bulk-copy engines).  Shape errors -> DIMENSION,
+ * aliasing.  sm_budget <= 0 means "whole GPU"; > 0 runs on at most that many
+ * SMs (one CTA per SM).  Shape errors -> DIMENSION,
  * eps < 0 or NaN -> NUMERIC (numerics.cpp:43-45). */
 TW_API tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* residual_out, void* output,
                               const float* weight, int64_t T, int64_t H, float eps, tw_dtype dtype,

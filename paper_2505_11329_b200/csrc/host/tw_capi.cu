@@ -360,7 +360,9 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
     // groups per SM double the per-SM rate of the pipeline (16.4 vs 18.5 us
     // at T=1024, 84.4 vs 85.4 us at 8192; H=6144: 65.6 vs 74 us; tools/k2_cps.py).
     static const char* cps_env = std::getenv("TW_K2_CTAS_PER_SM");
-    int cps = cps_env ? std::max(1, std::min(4, std::atoi(cps_env))) : 2;
+    // An explicit sm_budget keeps one CTA per SM (a ring larger than half the
+    // SM's shared memory cannot co-reside), so the budget really is SMs.
+    int cps = cps_env ? std::max(1, std::min(4, std::atoi(cps_env))) : (sm_budget > 0 ? 1 : 2);
     int stages = static_cast<int>(std::min<size_t>(8, (200 * 1024 / cps) / (2ull * row_bytes)));
     if (stages < 2 && cps > 1) {  // long rows (>= 25 KB): one CTA per SM keeps a 2+ stage ring
       cps = 1;
@@ -381,8 +383,7 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
       q.stages = stages;
       q.row_bytes = row_bytes;
       q.eps = eps;
-      // whole GPU: cps CTAs per SM; an explicit budget is a CTA count
-      const long long ctas = sm_budget > 0 ? sm_budget : static_cast<long long>(nsm) * cps;
+      const long long ctas = static_cast<long long>(sms) * cps;
       const int grid = static_cast<int>(std::min<long long>(T, ctas));
       cudaError_t e = launch_k2_bulk(q, bp.vpt, bf16, grid, static_cast<cudaStream_t>(stream), tma_store);
       if (e != cudaSuccess) return cuda_fail(e, "rmsnorm_residual (bulk) launch");
