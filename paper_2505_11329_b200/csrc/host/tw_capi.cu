@@ -360,9 +360,14 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
     // groups per SM double the per-SM rate of the pipeline (16.4 vs 18.5 us
     // at T=1024, 84.4 vs 85.4 us at 8192; H=6144: 65.6 vs 74 us; tools/k2_cps.py).
     static const char* cps_env = std::getenv("TW_K2_CTAS_PER_SM");
-    // An explicit sm_budget keeps one CTA per SM (a ring larger than half the
+    // Short batches (< ~48 rows per SM) use two CTAs per SM: two consumer
+    // groups per SM cut the pipeline-fill share (T=2048: 24.0 vs 29.1 us,
+    // 4096: 43.2 vs 47.2); long batches keep one CTA with the deeper ring
+    // (8192: 85.1 vs 86.5, 16384: 166.6 vs 172; tools/k2_cps_ab.py).  An
+    // explicit sm_budget keeps one CTA per SM (a ring larger than half the
     // SM's shared memory cannot co-reside), so the budget really is SMs.
-    int cps = cps_env ? std::max(1, std::min(4, std::atoi(cps_env))) : (sm_budget > 0 ? 1 : 2);
+    int cps = (sm_budget <= 0 && T < 48LL * nsm) ? 2 : 1;
+    if (cps_env) cps = std::max(1, std::min(4, std::atoi(cps_env)));
     int stages = static_cast<int>(std::min<size_t>(8, (200 * 1024 / cps) / (2ull * row_bytes)));
     if (stages < 2 && cps > 1) {  // long rows (>= 25 KB): one CTA per SM keeps a 2+ stage ring
       cps = 1;

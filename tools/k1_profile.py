@@ -17,7 +17,7 @@ ranges = tw.token_shard_map(T, W)
 shards = [torch.randn(e - b, H, device="cuda", dtype=torch.bfloat16) for b, e in ranges]
 w = [torch.ones(H, device="cuda")] * W
 for _ in range(int(os.environ.get("REPS", "3"))):
-    comm.fused_allreduce_rmsnorm(T, H, shards, w, sm_budget=148 // W)
+    comm.fused_allreduce_rmsnorm(T, H, shards, w, sm_budget=296 // W)
 torch.cuda.synchronize()
 comm.check()
 print("k1 profile workload done")

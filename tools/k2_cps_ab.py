@@ -1,0 +1,21 @@
+"""K2 TMA engine: 1 vs 2 CTAs per SM at larger T, bench methodology (mean of 50, write+read flush)."""
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        from bench import L2Flush, k2_timed
+        flush = L2Flush("cuda:0")
+        out = {}
+        for T in (2048, 4096, 6144, 8192, 12288, 16384):
+            ts, _ = k2_timed(T, 8192, 50, 5, flush)
+            out[T] = round(1e3 * sum(ts) / len(ts), 2)
+        print("cps", os.environ["TW_K2_CTAS_PER_SM"], out, flush=True)
+    else:
+        for rep in range(2):
+            for cps in ("1", "2"):
+                subprocess.run([sys.executable, __file__, "x"], env=dict(os.environ, TW_K2_CTAS_PER_SM=cps), check=True)
