@@ -356,9 +356,6 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
   if (vec && !want_rows) {
     RowPlan bp;
     const uint32_t row_bytes = static_cast<uint32_t>(H * (bf16 ? 2 : 4));
-    // Two CTAs per SM (each with half the shared-memory ring): two consumer
-    // groups per SM double the per-SM rate of the pipeline (16.4 vs 18.5 us
-    // at T=1024, 84.4 vs 85.4 us at 8192; H=6144: 65.6 vs 74 us; tools/k2_cps.py).
     static const char* cps_env = std::getenv("TW_K2_CTAS_PER_SM");
     // Short batches (< ~48 rows per SM) use two CTAs per SM: two consumer
     // groups per SM cut the pipeline-fill share (T=2048: 24.0 vs 29.1 us,
