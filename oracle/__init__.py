@@ -162,6 +162,7 @@ class RefLib:
         L.ref_make_split_plan.argtypes = [c_char_p, c_char_p, c_int64, _I64, _I64]
         L.ref_layer_latency.argtypes = [c_char_p, c_char_p, c_int64, c_char_p, POINTER(c_double)]
         L.ref_time_fused.argtypes = [c_int, c_int64, c_int64, c_int, c_int, POINTER(c_double)]
+        L.ref_calibrate_file.argtypes = [c_char_p, POINTER(c_double)]
         L.ref_time_rmsnorm.argtypes = [c_int64, c_int64, c_int, c_int, POINTER(c_double)]
         self.L = L
 
@@ -242,6 +243,16 @@ class RefLib:
         if st:
             raise StatusError(st, "ref_layer_latency")
         return s.value
+
+    def calibrate_file(self, path: str) -> dict:
+        """The reference calibrate() on a CalibrationTable JSON file."""
+        out = (c_double * 6)()
+        st = self.L.ref_calibrate_file(path.encode(), out)
+        if st:
+            raise StatusError(st, "ref_calibrate_file")
+        keys = ("ar_intercept_us", "ar_slope_us_per_token", "rmsnorm_intercept_us", "rmsnorm_slope_us_per_token",
+                "hbm_bandwidth_effective", "fused_extra_latency_s")
+        return dict(zip(keys, list(out)))
 
     def time_fused(self, world, T, H, parallel, iters) -> float:
         ms = c_double()

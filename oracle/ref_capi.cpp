@@ -14,6 +14,7 @@
 #include <thread>
 #include <vector>
 
+#include "weavesim/calibration.hpp"
 #include "weavesim/collectives.hpp"
 #include "weavesim/errors.hpp"
 #include "weavesim/numerics.hpp"
@@ -200,6 +201,29 @@ int ref_layer_latency(const char* profile, const char* model, std::int64_t T, co
     if (m == BaselineMode::TokenWeave && plan.mode != SplitMode::Overlap) m = BaselineMode::FuseOnly;
     std::vector<StreamEvent> g = build_layer_graph(plan, mp.spec, hp, m, 0);
     *seconds = simulate(g, hp).iteration_latency;
+  });
+}
+
+// The reference's own calibrate() (proj/src/calibration.cpp:98-192) on a
+// CalibrationTable JSON file: out6 = {AR intercept us, AR slope us/token,
+// RMSNorm intercept us, RMSNorm slope us/token, hbm_bandwidth_effective B/s,
+// fused_extra_latency s}.
+int ref_calibrate_file(const char* path, double* out6) {
+  return guarded([&] {
+    const CalibrationTable table = CalibrationTable::from_json_file(path);
+    HardwareProfile base;
+    base.name = "b200";
+    base.num_sms = 148;
+    base.sm_flops = 8.4e12;
+    const HardwareProfile p = calibrate(table, base);
+    out6[0] = p.collective_base_latency * 1e6;
+    out6[1] = p.collective_per_token_time * 1e6;
+    out6[2] = p.rmsnorm_base_latency * 1e6;
+    out6[3] = p.hbm_bandwidth_effective > 0 ? 3.0 * table.hidden * table.bytes_per_element /
+                                                  p.hbm_bandwidth_effective * 1e6
+                                            : 0.0;
+    out6[4] = p.hbm_bandwidth_effective;
+    out6[5] = p.fused_extra_latency;
   });
 }
 
