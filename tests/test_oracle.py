@@ -142,6 +142,25 @@ def test_oracle_matches_reference_split_planner(orc, ref):
             assert orc.smart_offset_analytic(T, sms, tile, cols) == ref.smart_offset_analytic(T, sms, tile, cols)
 
 
+def test_measured_calibration_table_feeds_reference_calibrate(ref):
+    """profiles/microbench_b200_measured.json parses with the
+    reference's CalibrationTable reader and calibrates: the measured K2 series
+    gives a smaller RMSNorm intercept and a higher effective HBM bandwidth
+    than the paper's table."""
+    import os
+    from tests.conftest import ROOT
+    path = os.path.join(ROOT, "profiles", "microbench_b200_measured.json")
+    if not os.path.exists(path):
+        pytest.skip("no measured table committed")
+    ours = ref.calibrate_file(path)
+    paper = ref.calibrate_file("/root/reference/proj/data/microbench_b200.json") if os.path.exists(
+        "/root/reference/proj/data/microbench_b200.json") else None
+    assert ours["rmsnorm_slope_us_per_token"] > 0 and ours["hbm_bandwidth_effective"] > 0
+    if paper:
+        assert ours["rmsnorm_intercept_us"] < paper["rmsnorm_intercept_us"]
+        assert ours["hbm_bandwidth_effective"] > paper["hbm_bandwidth_effective"]
+
+
 def test_oracle_error_codes_match_reference(orc, ref):
     x = np.ones((2, 4), np.float32)
     w = np.ones(4, np.float32)
