@@ -12,6 +12,12 @@ PKG := paper_2505_11329_b200
 LIBDIR := $(PKG)/lib
 OBJDIR := build/obj
 
+# Link the SYSTEM libstdc++.so.6 by name: a g++ wrapper whose own -B tree has a
+# dangling libstdc++.so symlink silently falls back to libstdc++.a, and a
+# static copy next to libtw.so's dynamic one corrupts iostream state (and
+# would split exception typeinfo across the drop-in boundary).
+STDCXX := -l:libstdc++.so.6
+
 KSRC := $(PKG)/csrc/kernels/tw_launch.cu
 HSRC := $(PKG)/csrc/host/tw_capi.cu
 MPSRC := $(PKG)/csrc/host/tw_mp.cu
@@ -50,13 +56,14 @@ $(LIBDIR)/libtw.so: $(OBJDIR)/tw_launch.o $(OBJDIR)/tw_capi.o $(OBJDIR)/tw_mp.o 
 shim: $(LIBDIR)/libweavesim_b200.so
 
 $(LIBDIR)/libweavesim_b200.so: $(SHIM_SRC) $(SHIM_HDR) $(LIBDIR)/libtw.so
-	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -o $@ $(SHIM_SRC) -L$(LIBDIR) -ltw -Wl,-rpath,'$$ORIGIN' -pthread
+	$(CXX) -std=c++20 -O2 -fPIC -shared -Iinclude -o $@ $(SHIM_SRC) -L$(LIBDIR) -ltw -Wl,-rpath,'$$ORIGIN' -pthread $(STDCXX)
 
 # The weave layer runner (links cuBLAS for the synthetic GEMM load).
 weave: $(LIBDIR)/libtw_weave.so
 
-$(LIBDIR)/libtw_weave.so: $(PKG)/csrc/weave/tw_weave.cu include/tw/tw_weave.h include/tw/tw.h $(LIBDIR)/libtw.so
-	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $< -L$(LIBDIR) -ltw -lcublas -Xlinker -rpath,'$$ORIGIN' \
+$(LIBDIR)/libtw_weave.so: $(PKG)/csrc/weave/tw_weave.cu include/tw/tw_weave.h include/tw/tw.h include/tw/tw_workload.h \
+                          $(LIBDIR)/libtw.so $(LIBDIR)/libweavesim_b200.so
+	$(NVCC) $(NVFLAGS) -shared -cudart static -o $@ $< -L$(LIBDIR) -ltw -lweavesim_b200 -lcublas -Xlinker -rpath,'$$ORIGIN' \
 	  -Xlinker -rpath,/usr/local/cuda/lib64 -Xlinker --exclude-libs,ALL
 
 # The reference's own test cases compiled against the drop-in library.
@@ -64,7 +71,7 @@ cpptests: build/tests/test_dropin
 
 build/tests/test_dropin: tests/cpp/test_dropin.cpp $(SHIM_HDR) $(LIBDIR)/libweavesim_b200.so
 	@mkdir -p build/tests
-	$(CXX) -std=c++20 -O2 -Iinclude -o $@ $< -L$(LIBDIR) -lweavesim_b200 -ltw -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)'
+	$(CXX) -std=c++20 -O2 -Iinclude -o $@ $< -L$(LIBDIR) -lweavesim_b200 -ltw -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' $(STDCXX)
 
 oracle:
 	$(MAKE) -C oracle oracle

@@ -41,7 +41,8 @@ typedef enum tw_status {
   TW_ERR_CONTRACT = 4,    /* weavesim::ContractError   errors.hpp:21  */
   TW_ERR_CUDA = 5,        /* CUDA runtime/driver failure              */
   TW_ERR_TIMEOUT = 6,     /* cross-rank barrier did not complete      */
-  TW_ERR_UNSUPPORTED = 7  /* e.g. NVLS requested on a non-NVSwitch box */
+  TW_ERR_UNSUPPORTED = 7, /* e.g. NVLS requested on a non-NVSwitch box */
+  TW_ERR_PARSE = 8        /* weavesim::ParseError      errors.hpp:26 (traces) */
 } tw_status;
 
 /* Activation storage type.  Weights are always fp32 (NormParams::weight is

@@ -23,6 +23,7 @@
 #define TW_TW_WEAVE_H
 
 #include "tw/tw.h"
+#include "tw/tw_workload.h"
 
 #ifdef __cplusplus
 extern "C" {
@@ -78,6 +79,38 @@ TW_API tw_status tw_weave_run(tw_weave_t w, int64_t T, int64_t prefix_tokens, tw
 TW_API tw_status tw_weave_run_ex(tw_weave_t w, int64_t T, int64_t prefix_tokens, tw_weave_mode mode,
                                  int boundary_sm_budget, int gemm_sm_target, int layers, unsigned flags,
                                  float* us_per_layer);
+
+/* tw_weave_run_ex for one serving batch: kv_context prior-context tokens
+ * (IterationBatch::kv_context, workloads.hpp:36) are attended from a synthetic
+ * KV cache -- 4*h*d*kv_context flops and kv_context*2*(kv_width/tp)*2 bytes,
+ * the reference's prior-context term (wavemodel.cpp:154-162); in WEAVE mode
+ * they divide between the splits in token proportion (scheduler.cpp:124-125). */
+TW_API tw_status tw_weave_run_batch(tw_weave_t w, int64_t T, int64_t prefix_tokens, int64_t kv_context,
+                                    tw_weave_mode mode, int boundary_sm_budget, int gemm_sm_target, int layers,
+                                    unsigned flags, float* us_per_layer);
+
+/* weavesim::ThroughputResult (workloads.hpp:41-48) without the latency vector. */
+typedef struct tw_throughput_result {
+  double tokens_per_sec;
+  int64_t iterations;
+  int64_t total_tokens;
+  double total_seconds;
+  double mean_iteration_latency;
+} tw_throughput_result;
+
+/* Measured serving throughput: the reference's simulate_throughput
+ * (proj/src/workloads.cpp:111-141) with every batch of form_batches(requests,
+ * chunk_size) RUN through tw_weave_run_batch (layers_measured chained layers
+ * after a warm-up layer) and its iteration latency = measured per-layer time x
+ * num_layers.  In WEAVE mode decode-only batches and batches make_split_plan
+ * (b200 geometry, threshold_tokens) does not split run FUSE_ONLY
+ * (scheduler.cpp:333-341).  iteration_latency_s (optional) receives up to
+ * max_iterations per-batch latencies in seconds. */
+TW_API tw_status tw_weave_throughput(tw_weave_t w, const tw_request* requests, int64_t n, int64_t chunk_size,
+                                     tw_weave_mode mode, int64_t threshold_tokens, int num_layers,
+                                     int layers_measured, int boundary_sm_budget, int gemm_sm_target,
+                                     unsigned flags, tw_throughput_result* result, double* iteration_latency_s,
+                                     int64_t max_iterations);
 
 /* Per-event timestamps (us from the run's start) of the LAST layer of the
  * last tw_weave_run: op (tw_weave_op), split (0 prefix, 1 suffix, 2 whole),

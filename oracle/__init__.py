@@ -61,6 +61,8 @@ class Oracle:
         L.orc_make_split_plan.argtypes = [c_int64, c_int64, c_int64, c_int64, c_int64, _I64]
         L.orc_place_sequence_boundaries.argtypes = [_I64, c_int, c_int64, c_int64, _I64]
         L.orc_round_to_bf16.argtypes = [_F, _F, c_int64]
+        _D = POINTER(c_double)
+        L.orc_form_batches.argtypes = [_I64, _I64, _D, c_int64, c_int64, _I64, c_int64, _I64, c_int64, _I64]
         self.L = L
 
     def token_shard_map(self, T: int, world: int):
@@ -132,6 +134,24 @@ class Oracle:
             raise StatusError(st, "place_sequence_boundaries")
         return list(out)[:n]
 
+    def form_batches(self, requests, chunk_size):
+        """requests: [(prompt, output, arrival_s)] -> [(total, decode, kv, [(id, start, len)])]."""
+        n = len(requests)
+        pr = (c_int64 * max(n, 1))(*[r[0] for r in requests])
+        ou = (c_int64 * max(n, 1))(*[r[1] for r in requests])
+        ar = (c_double * max(n, 1))(*[float(r[2]) if len(r) > 2 else 0.0 for r in requests])
+        counts = (c_int64 * 2)()
+        st = self.L.orc_form_batches(pr, ou, ar, n, chunk_size, None, 0, None, 0, counts)
+        if st not in (0, 1):
+            raise StatusError(st, "form_batches")
+        nb, ns = counts[0], counts[1]
+        out4 = (c_int64 * (4 * max(nb, 1)))()
+        sl3 = (c_int64 * (3 * max(ns, 1)))()
+        st = self.L.orc_form_batches(pr, ou, ar, n, chunk_size, out4, nb, sl3, ns, counts)
+        if st:
+            raise StatusError(st, "form_batches")
+        return _unpack_batches(out4, sl3, nb)
+
     def round_bf16(self, a: np.ndarray) -> np.ndarray:
         a = np.ascontiguousarray(a, np.float32)
         out = np.empty_like(a)
@@ -164,6 +184,11 @@ class RefLib:
         L.ref_time_fused.argtypes = [c_int, c_int64, c_int64, c_int, c_int, POINTER(c_double)]
         L.ref_calibrate_file.argtypes = [c_char_p, POINTER(c_double)]
         L.ref_time_rmsnorm.argtypes = [c_int64, c_int64, c_int, c_int, POINTER(c_double)]
+        _D = POINTER(c_double)
+        L.ref_form_batches.argtypes = [_I64, _D, c_int64, c_int64, _I64, c_int64, _I64, c_int64, _I64]
+        L.ref_save_trace.argtypes = [_I64, _D, c_int64, c_char_p]
+        L.ref_load_trace.argtypes = [c_char_p, _I64, _D, c_int64, _I64]
+        L.ref_simulate_throughput.argtypes = [c_char_p, c_char_p, c_char_p, _I64, c_int64, c_int64, _D]
         self.L = L
 
     def rmsnorm_residual(self, inp, res, weight, eps=1e-5):
@@ -267,6 +292,66 @@ class RefLib:
         if st:
             raise StatusError(st, "ref_time_rmsnorm")
         return ms.value
+
+    @staticmethod
+    def _req_arrays(requests):
+        n = len(requests)
+        r2 = (c_int64 * (2 * max(n, 1)))(*[v for r in requests for v in (r[0], r[1])])
+        ar = (c_double * max(n, 1))(*[float(r[2]) if len(r) > 2 else 0.0 for r in requests])
+        return n, r2, ar
+
+    def form_batches(self, requests, chunk_size):
+        """weavesim::form_batches itself; same return shape as Oracle.form_batches."""
+        n, r2, ar = self._req_arrays(requests)
+        counts = (c_int64 * 2)()
+        st = self.L.ref_form_batches(r2, ar, n, chunk_size, (c_int64 * 4)(), 0, (c_int64 * 3)(), 0, counts)
+        if st not in (0, 1):
+            raise StatusError(st, "ref_form_batches")
+        nb, ns = counts[0], counts[1]
+        out4 = (c_int64 * (4 * max(nb, 1)))()
+        sl3 = (c_int64 * (3 * max(ns, 1)))()
+        st = self.L.ref_form_batches(r2, ar, n, chunk_size, out4, nb, sl3, ns, counts)
+        if st:
+            raise StatusError(st, "ref_form_batches")
+        return _unpack_batches(out4, sl3, nb)
+
+    def save_trace(self, requests, path: str) -> None:
+        n, r2, ar = self._req_arrays(requests)
+        st = self.L.ref_save_trace(r2, ar, n, path.encode())
+        if st:
+            raise StatusError(st, "ref_save_trace")
+
+    def load_trace(self, path: str):
+        """[(prompt, output, arrival_s)]; StatusError(5) is the reference ParseError."""
+        cnt = c_int64()
+        st = self.L.ref_load_trace(path.encode(), None, None, 0, ctypes.byref(cnt))
+        if st:
+            raise StatusError(st, "ref_load_trace")
+        n = cnt.value
+        r2 = (c_int64 * (2 * max(n, 1)))()
+        ar = (c_double * max(n, 1))()
+        self.L.ref_load_trace(path.encode(), r2, ar, n, ctypes.byref(cnt))
+        return [(r2[2 * i], r2[2 * i + 1], ar[i]) for i in range(n)]
+
+    def simulate_throughput(self, profile, model, mode, requests, chunk_size) -> dict:
+        """The reference's MODELED throughput (scheduler + wave model)."""
+        n, r2, _ = self._req_arrays(requests)
+        out = (c_double * 4)()
+        st = self.L.ref_simulate_throughput(profile.encode(), model.encode(), mode.encode(), r2, n, chunk_size, out)
+        if st:
+            raise StatusError(st, "ref_simulate_throughput")
+        return {"tokens_per_sec": out[0], "iterations": int(out[1]), "total_tokens": int(out[2]),
+                "total_seconds": out[3]}
+
+
+def _unpack_batches(out4, sl3, nb):
+    batches, s = [], 0
+    for k in range(nb):
+        ns = out4[4 * k + 3]
+        slices = [(sl3[3 * j], sl3[3 * j + 1], sl3[3 * j + 2]) for j in range(s, s + ns)]
+        s += ns
+        batches.append((out4[4 * k], out4[4 * k + 1], out4[4 * k + 2], slices))
+    return batches
 
 
 def bf16_round(a: np.ndarray) -> np.ndarray:

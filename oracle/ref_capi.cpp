@@ -22,6 +22,7 @@
 #include "weavesim/scheduler.hpp"
 #include "weavesim/splitter.hpp"
 #include "weavesim/wavemodel.hpp"
+#include "weavesim/workloads.hpp"
 
 using namespace weavesim;
 
@@ -300,6 +301,85 @@ int ref_time_rmsnorm(std::int64_t T, std::int64_t H, int threads, int iters, dou
     }
     std::sort(ms.begin(), ms.end());
     *median_ms = ms[ms.size() / 2];
+  });
+}
+
+// --- Workloads (proj/src/workloads.cpp): traces, form_batches, the modeled
+// throughput (simulate_throughput) that the measured run is printed beside.
+// Requests are flat int64 triples {prompt, output, arrival_us} (id = index).
+
+namespace {
+std::vector<Request> make_requests(const std::int64_t* r3, const double* arrival, std::int64_t n) {
+  std::vector<Request> v;
+  for (std::int64_t i = 0; i < n; ++i) v.push_back({i, r3[2 * i], r3[2 * i + 1], arrival ? arrival[i] : 0.0});
+  return v;
+}
+}  // namespace
+
+// out rows: {total_tokens, decode_token_count, kv_context, num_slices}; slices
+// rows: {request_id, start, len}.  counts[2] = {batches, slices} (always set);
+// returns 1 (DimensionError) if the arrays are too small.
+int ref_form_batches(const std::int64_t* r2, const double* arrival, std::int64_t n, std::int64_t chunk,
+                     std::int64_t* out4, std::int64_t max_batches, std::int64_t* slices3, std::int64_t max_slices,
+                     std::int64_t* counts) {
+  return guarded([&] {
+    const std::vector<IterationBatch> b = form_batches(make_requests(r2, arrival, n), chunk);
+    std::int64_t ns = 0;
+    for (const auto& x : b) ns += static_cast<std::int64_t>(x.prefill_token_slices.size());
+    counts[0] = static_cast<std::int64_t>(b.size());
+    counts[1] = ns;
+    if (counts[0] > max_batches || ns > max_slices) throw DimensionError("too small");
+    std::int64_t s = 0;
+    for (std::size_t k = 0; k < b.size(); ++k) {
+      out4[4 * k + 0] = b[k].total_tokens;
+      out4[4 * k + 1] = b[k].decode_token_count;
+      out4[4 * k + 2] = b[k].kv_context;
+      out4[4 * k + 3] = static_cast<std::int64_t>(b[k].prefill_token_slices.size());
+      for (const auto& p : b[k].prefill_token_slices) {
+        slices3[3 * s + 0] = p.request_id;
+        slices3[3 * s + 1] = p.start;
+        slices3[3 * s + 2] = p.len;
+        ++s;
+      }
+    }
+  });
+}
+
+int ref_save_trace(const std::int64_t* r2, const double* arrival, std::int64_t n, const char* path) {
+  return guarded([&] { save_trace(make_requests(r2, arrival, n), path); });
+}
+
+// counts = number of requests; r2/arrival filled up to cap.  ParseError -> 5.
+int ref_load_trace(const char* path, std::int64_t* r2, double* arrival, std::int64_t cap, std::int64_t* count) {
+  try {
+    const std::vector<Request> v = load_trace(path);
+    *count = static_cast<std::int64_t>(v.size());
+    for (std::int64_t i = 0; i < std::min<std::int64_t>(cap, *count); ++i) {
+      r2[2 * i] = v[i].prompt_tokens;
+      r2[2 * i + 1] = v[i].output_tokens;
+      arrival[i] = v[i].arrival_s;
+    }
+    return 0;
+  } catch (const ParseError&) {
+    return 5;
+  } catch (...) {
+    return 9;
+  }
+}
+
+// simulate_throughput on a builtin profile/model preset: out4 = {tokens_per_sec,
+// iterations, total_tokens, total_seconds}.
+int ref_simulate_throughput(const char* profile, const char* model, const char* mode, const std::int64_t* r2,
+                            std::int64_t n, std::int64_t chunk, double* out4) {
+  return guarded([&] {
+    const HardwareProfile hp = builtin_profile(profile);
+    const ModelPreset mp = model_preset(model);
+    const ThroughputResult r = simulate_throughput(make_requests(r2, nullptr, n), mp.spec, hp,
+                                                   baseline_mode_from_string(mode), mp.policy, chunk);
+    out4[0] = r.tokens_per_sec;
+    out4[1] = static_cast<double>(r.iterations);
+    out4[2] = static_cast<double>(r.total_tokens);
+    out4[3] = r.total_seconds;
   });
 }
 

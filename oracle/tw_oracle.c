@@ -230,3 +230,78 @@ void orc_f32_to_bf16_bits(const float* in, uint16_t* out, int64_t n) {
 void orc_bf16_bits_to_f32(const uint16_t* in, float* out, int64_t n) {
   for (int64_t i = 0; i < n; ++i) out[i] = bf16_to_f32(in[i]);
 }
+
+/* ---- form_batches  proj/src/workloads.cpp:68-109 --------------------------------
+ * A literal restatement: every iteration rescans the FCFS order twice (decode
+ * pass :86-95, prefill pass :96-107); the stable sort by arrival (:76-80) is an
+ * insertion sort (stable, ties keep index order). */
+int orc_form_batches(const int64_t* prompt, const int64_t* output, const double* arrival, int64_t n,
+                     int64_t chunk_size, int64_t* out4, int64_t max_batches, int64_t* slices3,
+                     int64_t max_slices, int64_t* counts) {
+  if (chunk_size < 1) return 3;
+  int64_t* order = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+  int64_t* prefilled = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
+  int64_t* decoded = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t j = i;
+    while (j > 0 && (arrival ? arrival[order[j - 1]] : 0.0) > (arrival ? arrival[i] : 0.0)) {
+      order[j] = order[j - 1];
+      --j;
+    }
+    order[j] = i;
+  }
+  int64_t nb = 0, ns = 0;
+  int overflow = 0;
+  for (;;) {
+    int64_t decode = 0, kv = 0, total = 0, first = ns, nslice = 0;
+    for (int64_t k = 0; k < n; ++k) {
+      const int64_t i = order[k];
+      if (prefilled[i] == prompt[i] && decoded[i] < output[i]) {
+        ++decoded[i];
+        ++decode;
+        kv += prompt[i] + decoded[i] - 1;
+      }
+    }
+    int64_t budget = chunk_size - decode;
+    for (int64_t k = 0; k < n; ++k) {
+      if (budget <= 0) break;
+      const int64_t i = order[k];
+      if (prefilled[i] == prompt[i]) continue;
+      const int64_t left = prompt[i] - prefilled[i];
+      const int64_t take = budget < left ? budget : left;
+      if (ns < max_slices) {
+        slices3[3 * ns + 0] = i;
+        slices3[3 * ns + 1] = prefilled[i];
+        slices3[3 * ns + 2] = take;
+      } else {
+        overflow = 1;
+      }
+      ++ns;
+      ++nslice;
+      kv += prefilled[i];
+      prefilled[i] += take;
+      budget -= take;
+      total += take;
+    }
+    total += decode;
+    if (total == 0) {
+      ns = first;
+      break;
+    }
+    if (nb < max_batches) {
+      out4[4 * nb + 0] = total;
+      out4[4 * nb + 1] = decode;
+      out4[4 * nb + 2] = kv;
+      out4[4 * nb + 3] = nslice;
+    } else {
+      overflow = 1;
+    }
+    ++nb;
+  }
+  counts[0] = nb;
+  counts[1] = ns;
+  free(order);
+  free(prefilled);
+  free(decoded);
+  return overflow ? 1 : 0;
+}

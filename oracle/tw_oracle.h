@@ -71,6 +71,15 @@ int orc_make_split_plan(int64_t num_tokens, int64_t threshold, int64_t num_sms,
 int orc_place_sequence_boundaries(const int64_t* lengths, int n, int64_t total_tokens,
                                   int64_t prefix_tokens, int64_t* prefix_len_out);
 
+/* form_batches  proj/src/workloads.cpp:68-109 (FCFS chunked prefill,
+ * decode first).  Requests: prompt[n], output[n], arrival[n] (id = index).
+ * out4 rows {total_tokens, decode_token_count, kv_context, num_slices};
+ * slices3 rows {request_id, start, len}.  counts = {batches, slices} (always
+ * set).  Returns 0, 3 (chunk_size < 1) or 1 (arrays too small). */
+int orc_form_batches(const int64_t* prompt, const int64_t* output, const double* arrival, int64_t n,
+                     int64_t chunk_size, int64_t* out4, int64_t max_batches, int64_t* slices3,
+                     int64_t max_slices, int64_t* counts);
+
 /* bf16 round-to-nearest-even helpers (the GPU's storage format). */
 void orc_round_to_bf16(const float* in, float* out, int64_t n);
 void orc_f32_to_bf16_bits(const float* in, uint16_t* out, int64_t n);

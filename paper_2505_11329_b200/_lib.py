@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libtw.so")
 
 TW_OK, TW_ERR_DIMENSION, TW_ERR_NUMERIC, TW_ERR_CONFIG, TW_ERR_CONTRACT, TW_ERR_CUDA, TW_ERR_TIMEOUT, \
-    TW_ERR_UNSUPPORTED = range(8)
+    TW_ERR_UNSUPPORTED, TW_ERR_PARSE = range(9)
 TW_BF16, TW_F32 = 0, 1
 TW_TRANSPORT_AUTO, TW_TRANSPORT_NVLS, TW_TRANSPORT_PEER = 0, 1, 2
 TW_BUF_INPUT, TW_BUF_OUTPUT, TW_BUF_RESIDUAL = 0, 1, 2
@@ -54,6 +54,10 @@ class Unsupported(TwError):
     pass
 
 
+class ParseError(TwError):
+    pass
+
+
 _ERRORS = {
     TW_ERR_DIMENSION: DimensionError,
     TW_ERR_NUMERIC: NumericError,
@@ -62,6 +66,7 @@ _ERRORS = {
     TW_ERR_CUDA: CudaError,
     TW_ERR_TIMEOUT: BarrierTimeout,
     TW_ERR_UNSUPPORTED: Unsupported,
+    TW_ERR_PARSE: ParseError,
 }
 
 # (name, restype, argtypes) for every symbol tw.h declares.
@@ -116,9 +121,12 @@ def _load() -> ctypes.CDLL:
 lib = _load()
 
 
-def check(status: int) -> None:
+def check(status: int, message=None) -> None:
+    """Raise the taxonomy's exception for a failing status; `message` is a
+    callable returning the layer's last-error text (default: libtw's)."""
     if status != TW_OK:
-        msg = (lib.tw_last_error() or b"").decode()
+        raw = message() if message is not None else lib.tw_last_error()
+        msg = (raw or b"").decode()
         raise _ERRORS.get(status, TwError)(msg or f"tw status {status}")
 
 

@@ -15,7 +15,9 @@
 #include <vector>
 
 #include "tw/tw.h"
+#include "tw/tw_split.h"
 #include "tw/tw_weave.h"
+#include "tw/tw_workload.h"
 
 namespace {
 
@@ -79,6 +81,12 @@ struct tw_weave {
   int rank = 0, world = 1;
   void* X_local = nullptr;  // TP=1 / unfused-baseline hidden buffer
   void* X_comm = nullptr;   // comm OUTPUT
+  // Prior-context attention (serving batches, tw_weave_run_batch): a synthetic
+  // KV cache of kv_cap tokens x this GPU's KV heads, its score scratch and the
+  // context output.  Grown on demand outside timed regions.
+  int64_t kv_context = 0;
+  int64_t kv_cap = 0;
+  void *KV = nullptr, *SC = nullptr, *CO = nullptr;
 };
 
 namespace {
@@ -132,7 +140,14 @@ void op_end(tw_weave* w, size_t id, cudaStream_t s) {
 // heads of this GPU with L = kv_prior + n/2 keys (flops = 4*h*d*(n^2/2 +
 // n*kv_prior), proj/src/wavemodel.cpp:150-153), and the O projection into
 // the partial-sum buffer P (the tensor the boundary op all-reduces).
-tw_status attention(tw_weave* w, int64_t r0, int64_t n, int64_t kv_prior) {
+//
+// kv_ctx > 0 adds attention over kv_ctx cached prior-context tokens (decode
+// tokens' histories, earlier prefill chunks): per KV head of this GPU one
+// [g x d] x [d x kv_ctx] and one [g x kv_ctx] x [kv_ctx x d] GEMM (g = query
+// heads per KV head), i.e. 4*h*d*kv_ctx flops and kv_ctx*2*(kv_width/tp)*2
+// bytes of K/V streamed from HBM -- the reference's prior-context term
+// (wavemodel.cpp:154-162, scheduler.cpp:72-83).
+tw_status attention(tw_weave* w, int64_t r0, int64_t n, int64_t kv_prior, int64_t kv_ctx = 0) {
   if (n <= 0) return TW_OK;
   const tw_layer_spec& sp = w->spec;
   const int64_t H = sp.hidden, d = sp.head_dim;
@@ -149,8 +164,43 @@ tw_status attention(tw_weave* w, int64_t r0, int64_t n, int64_t kv_prior) {
   // out[h] = scores[h] [n x L] * V_h [L x d]
   CUBLAS_TRY(gemm_rm(w->blas, n, d, L, w->S, L, n * L, QKV, d, L * d, A + r0 * (w->hg * d) * kBf16, w->hg * d, d,
                      static_cast<int>(w->hg)));
+  if (kv_ctx > 0) {
+    const int64_t kvh = std::max<int64_t>(1, sp.kv_heads / sp.tp), g = w->hg / kvh;
+    char* K = static_cast<char*>(w->KV);
+    char* V = K + kv_ctx * kvh * d * kBf16;
+    // scores[k] = Q_k [g x d] * K_k [d x kv]; out[k] = scores[k] [g x kv] * V_k [kv x d]
+    CUBLAS_TRY(gemm_rm(w->blas, g, kv_ctx, d, QKV + r0 * w->qkvw * kBf16, d, g * d, K, kv_ctx, d * kv_ctx, w->SC,
+                       kv_ctx, g * kv_ctx, static_cast<int>(kvh)));
+    CUBLAS_TRY(gemm_rm(w->blas, g, d, kv_ctx, w->SC, kv_ctx, g * kv_ctx, V, d, kv_ctx * d, w->CO, d, g * d,
+                       static_cast<int>(kvh)));
+  }
   CUBLAS_TRY(gemm_rm(w->blas, n, H, w->hg * d, A + r0 * (w->hg * d) * kBf16, w->hg * d, 0, w->Wo, H, 0,
                      P + r0 * H * kBf16, H, 0, 1));
+  return TW_OK;
+}
+
+// Grow the KV cache / score scratch to hold kv tokens of context.
+tw_status ensure_context(tw_weave* w, int64_t kv) {
+  if (kv <= w->kv_cap) return TW_OK;
+  const tw_layer_spec& sp = w->spec;
+  const int64_t d = sp.head_dim, kvh = std::max<int64_t>(1, sp.kv_heads / sp.tp), g = w->hg / kvh;
+  const int64_t cap = std::max<int64_t>(kv, 2 * w->kv_cap);
+  CUDA_TRY(cudaStreamSynchronize(w->compute));
+  CUDA_TRY(cudaStreamSynchronize(w->boundary));
+  for (void** p : {&w->KV, &w->SC, &w->CO})
+    if (*p) {
+      cudaFree(*p);
+      *p = nullptr;
+    }
+  w->kv_cap = 0;
+  const size_t sizes[3] = {size_t(2 * cap * kvh * d * kBf16), size_t(kvh * g * cap * kBf16),
+                           size_t(kvh * g * d * kBf16)};
+  void** ptrs[3] = {&w->KV, &w->SC, &w->CO};
+  for (int i = 0; i < 3; ++i) {
+    CUDA_TRY(cudaMalloc(ptrs[i], sizes[i]));
+    CUDA_TRY(cudaMemset(*ptrs[i], 0, sizes[i]));
+  }
+  w->kv_cap = cap;
   return TW_OK;
 }
 
@@ -372,6 +422,8 @@ tw_status tw_weave_destroy(tw_weave_t w) {
                   w->Wup, w->Wdown, w->wnorm};  // P / X_comm belong to the communicator in TP mode
   for (void* b : bufs)
     if (b) cudaFree(b);
+  for (void* b : {w->KV, w->SC, w->CO})
+    if (b) cudaFree(b);
   for (Ev& e : w->pool) {
     cudaEventDestroy(e.start);
     cudaEventDestroy(e.end);
@@ -399,7 +451,7 @@ tw_status layer(tw_weave* w, int64_t T, int64_t ta, tw_weave_mode mode, int budg
     // Sequential chain on one stream: attn -> fused -> ffn -> fused.
     if (carry_a) CUDA_TRY(cudaStreamWaitEvent(cs, carry_a, 0));
     size_t id = op_begin(w, TW_OP_ATTENTION, 2, 0, cs);
-    TW_TRY(attention(w, 0, T, 0));
+    TW_TRY(attention(w, 0, T, 0, w->kv_context));
     op_end(w, id, cs);
     if (mode == TW_MODE_FUSE_ONLY || mode == TW_MODE_UNFUSED) {
       id = op_begin(w, TW_OP_FUSED, 2, 0, cs);
@@ -420,10 +472,12 @@ tw_status layer(tw_weave* w, int64_t T, int64_t ta, tw_weave_mode mode, int budg
     return TW_OK;
   }
   const int64_t tb = T - ta;
+  // prior context divides between the splits in token proportion (scheduler.cpp:124-125)
+  const int64_t kv_a = w->kv_context * ta / T, kv_b = w->kv_context - kv_a;
   // compute: attn(a)
   if (carry_a) CUDA_TRY(cudaStreamWaitEvent(cs, carry_a, 0));
   size_t id = op_begin(w, TW_OP_ATTENTION, 0, 0, cs);
-  TW_TRY(attention(w, 0, ta, 0));
+  TW_TRY(attention(w, 0, ta, 0, kv_a));
   op_end(w, id, cs);
   cudaEvent_t e_aa = edge(w);
   CUDA_TRY(cudaEventRecord(e_aa, cs));
@@ -437,7 +491,7 @@ tw_status layer(tw_weave* w, int64_t T, int64_t ta, tw_weave_mode mode, int budg
   // compute: attn(b) -- chunked-attention edge: keys include the prefix
   if (carry_b) CUDA_TRY(cudaStreamWaitEvent(cs, carry_b, 0));
   id = op_begin(w, TW_OP_ATTENTION, 1, 0, cs);
-  TW_TRY(attention(w, ta, tb, ta));
+  TW_TRY(attention(w, ta, tb, ta, kv_b));
   op_end(w, id, cs);
   cudaEvent_t e_ab = edge(w);
   CUDA_TRY(cudaEventRecord(e_ab, cs));
@@ -521,7 +575,11 @@ tw_status run_graph(tw_weave* w, int64_t T, int64_t prefix, tw_weave_mode mode, 
     e = cudaStreamEndCapture(w->compute, &graph);
     if (st == TW_OK && e != cudaSuccess) st = werr(TW_ERR_CUDA, std::string("end capture: ") + cudaGetErrorString(e));
     if (st == TW_OK) {
-      e = cudaGraphInstantiate(&exec, graph, 0);
+      // Per-node priorities: captured kernel nodes carry their stream's
+      // priority, but a graph runs every node at the LAUNCH stream's priority
+      // (the low-priority compute stream) unless told otherwise -- which
+      // would demote the boundary op behind the GEMMs.
+      e = cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority);
       if (e != cudaSuccess) st = werr(TW_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
     }
   }
@@ -558,7 +616,18 @@ tw_status tw_weave_run(tw_weave_t w, int64_t T, int64_t prefix_tokens, tw_weave_
 
 tw_status tw_weave_run_ex(tw_weave_t w, int64_t T, int64_t prefix_tokens, tw_weave_mode mode, int boundary_sm_budget,
                           int gemm_sm_target, int layers, unsigned flags, float* us_per_layer) {
+  return tw_weave_run_batch(w, T, prefix_tokens, 0, mode, boundary_sm_budget, gemm_sm_target, layers, flags,
+                            us_per_layer);
+}
+
+tw_status tw_weave_run_batch(tw_weave_t w, int64_t T, int64_t prefix_tokens, int64_t kv_context, tw_weave_mode mode,
+                             int boundary_sm_budget, int gemm_sm_target, int layers, unsigned flags,
+                             float* us_per_layer) {
   if (!w || !us_per_layer) return werr(TW_ERR_CONFIG, "weave_run: null argument");
+  if (kv_context < 0) return werr(TW_ERR_DIMENSION, "weave_run: negative kv_context");
+  CUDA_TRY(cudaSetDevice(w->device));
+  if (tw_status st = ensure_context(w, kv_context)) return st;
+  w->kv_context = kv_context;
   if (flags & TW_WEAVE_CUDA_GRAPH) return run_graph(w, T, prefix_tokens, mode, boundary_sm_budget, gemm_sm_target,
                                                     layers, us_per_layer);
   if (T < 1 || T > w->max_tokens) return werr(TW_ERR_DIMENSION, "weave_run: T out of range");
@@ -625,6 +694,61 @@ tw_status tw_weave_trace(tw_weave_t w, int max_events, int* n_events, int* op, i
     if (start_us) start_us[i] = 1000.0f * a;
     if (end_us) end_us[i] = 1000.0f * b;
   }
+  return TW_OK;
+}
+
+// Serving throughput on measured layers: the reference's simulate_throughput
+// (workloads.cpp:111-141) with each batch RUN instead of priced.  Batches come
+// from form_batches (FCFS chunked prefill, decode first); in TokenWeave mode a
+// batch overlaps only if it has prefill tokens and make_split_plan (b200
+// geometry, the model's threshold) says Overlap -- otherwise it runs fuse-only,
+// as iteration_timeline degrades it (scheduler.cpp:333-341).
+tw_status tw_weave_throughput(tw_weave_t w, const tw_request* requests, int64_t n, int64_t chunk_size,
+                              tw_weave_mode mode, int64_t threshold_tokens, int num_layers, int layers_measured,
+                              int boundary_sm_budget, int gemm_sm_target, unsigned flags,
+                              tw_throughput_result* result, double* iteration_latency_s, int64_t max_iterations) {
+  if (!w || !result) return werr(TW_ERR_CONFIG, "weave_throughput: null argument");
+  if (num_layers < 1 || layers_measured < 1) return werr(TW_ERR_CONFIG, "weave_throughput: layer counts must be >= 1");
+  int64_t nb = 0, ns = 0;
+  tw_status st = tw_form_batches(requests, n, chunk_size, nullptr, 0, nullptr, 0, &nb, &ns);
+  if (st != TW_OK && st != TW_ERR_DIMENSION) return werr(st, std::string("form_batches: ") + tw_workload_last_error());
+  std::vector<tw_iteration_batch> batches(static_cast<size_t>(std::max<int64_t>(nb, 1)));
+  std::vector<tw_prefill_slice> slices(static_cast<size_t>(std::max<int64_t>(ns, 1)));
+  st = tw_form_batches(requests, n, chunk_size, batches.data(), nb, slices.data(), ns, &nb, &ns);
+  if (st != TW_OK) return werr(st, std::string("form_batches: ") + tw_workload_last_error());
+  *result = tw_throughput_result{};
+  for (int64_t k = 0; k < nb; ++k) {
+    const tw_iteration_batch& b = batches[static_cast<size_t>(k)];
+    if (b.total_tokens > w->max_tokens)
+      return werr(TW_ERR_DIMENSION, "weave_throughput: batch of " + std::to_string(b.total_tokens) +
+                                        " tokens exceeds the runner's max_tokens");
+    tw_weave_mode m = mode;
+    int64_t prefix = 0;
+    if (mode == TW_MODE_WEAVE) {
+      m = TW_MODE_FUSE_ONLY;
+      if (b.num_slices > 0) {
+        int64_t a = 0, bb = 0, off = 0;
+        int pm = 0;
+        st = tw_make_split_plan(b.total_tokens, 148, 128, 32, threshold_tokens, &a, &bb, &off, &pm);
+        if (st != TW_OK) return werr(st, "weave_throughput: make_split_plan failed");
+        if (pm == 2 && bb > 0) {
+          m = TW_MODE_WEAVE;
+          prefix = a;
+        }
+      }
+    }
+    float us = 0.0f;
+    st = tw_weave_run_batch(w, b.total_tokens, prefix, b.kv_context, m, boundary_sm_budget, gemm_sm_target,
+                            layers_measured, flags, &us);
+    if (st != TW_OK) return st;
+    const double lat = 1e-6 * static_cast<double>(us) * num_layers;
+    if (iteration_latency_s && k < max_iterations) iteration_latency_s[k] = lat;
+    result->total_seconds += lat;
+    result->total_tokens += b.total_tokens;
+  }
+  result->iterations = nb;
+  if (result->total_seconds > 0.0) result->tokens_per_sec = result->total_tokens / result->total_seconds;
+  if (nb > 0) result->mean_iteration_latency = result->total_seconds / static_cast<double>(nb);
   return TW_OK;
 }
 

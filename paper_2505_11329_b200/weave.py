@@ -57,13 +57,94 @@ def _split_lib():
     lib.tw_smart_offset_analytic.argtypes = [c_int64, c_int, c_int, c_int, POINTER(c_int64)]
     lib.tw_smart_offset_sweep.argtypes = [c_int64, POINTER(c_int64), c_int, _FWD, c_void_p, POINTER(c_int64)]
     lib.tw_place_sequence_boundaries.argtypes = [POINTER(c_int64), c_int, c_int64, c_int64, POINTER(c_int64)]
+    lib.tw_workload_last_error.restype = ctypes.c_char_p
+    lib.tw_workload_last_error.argtypes = []
+    lib.tw_synth_trace.argtypes = [c_int64, c_int64, c_int64, POINTER(Request)]
+    lib.tw_load_trace.argtypes = [ctypes.c_char_p, POINTER(Request), c_int64, POINTER(c_int64)]
+    lib.tw_save_trace.argtypes = [POINTER(Request), c_int64, ctypes.c_char_p]
+    lib.tw_form_batches.argtypes = [POINTER(Request), c_int64, c_int64, POINTER(IterationBatch), c_int64,
+                                    POINTER(PrefillSlice), c_int64, POINTER(c_int64), POINTER(c_int64)]
     for f in ("tw_make_split_plan", "tw_smart_offset_analytic", "tw_smart_offset_sweep",
-              "tw_place_sequence_boundaries"):
+              "tw_place_sequence_boundaries", "tw_synth_trace", "tw_load_trace", "tw_save_trace",
+              "tw_form_batches"):
         getattr(lib, f).restype = c_int
     return lib
 
 
+class Request(Structure):
+    """tw_request = weavesim::Request (workloads.hpp:12-17)."""
+    _fields_ = [("id", c_int64), ("prompt_tokens", c_int64), ("output_tokens", c_int64), ("arrival_s", c_double)]
+
+
+class PrefillSlice(Structure):
+    _fields_ = [("request_id", c_int64), ("start", c_int64), ("len", c_int64)]
+
+
+class IterationBatch(Structure):
+    _fields_ = [("total_tokens", c_int64), ("decode_token_count", c_int64), ("kv_context", c_int64),
+                ("first_slice", c_int64), ("num_slices", c_int64)]
+
+
+class ThroughputResult(Structure):
+    _fields_ = [("tokens_per_sec", c_double), ("iterations", c_int64), ("total_tokens", c_int64),
+                ("total_seconds", c_double), ("mean_iteration_latency", c_double)]
+
+
 _S = _split_lib()
+
+
+def _wcheck(status: int) -> None:
+    check(status, _S.tw_workload_last_error)
+
+
+def _requests(requests):
+    """[(prompt, output[, arrival_s])] or Request structs -> a tw_request array."""
+    arr = (Request * max(len(requests), 1))()
+    for i, r in enumerate(requests):
+        if isinstance(r, Request):
+            arr[i] = r
+        else:
+            arr[i] = Request(i, r[0], r[1], float(r[2]) if len(r) > 2 else 0.0)
+    return arr
+
+
+def synth_trace(count: int, prompt_len: int, output_len: int):
+    """weavesim::synth_trace -> [(prompt, output, arrival_s)]."""
+    arr = (Request * max(count, 1))()
+    _wcheck(_S.tw_synth_trace(count, prompt_len, output_len, arr))
+    return [(arr[i].prompt_tokens, arr[i].output_tokens, arr[i].arrival_s) for i in range(count)]
+
+
+def load_trace(path: str):
+    """weavesim::load_trace (JSONL) -> [(prompt, output, arrival_s)]; ParseError like the reference."""
+    n = c_int64()
+    _wcheck(_S.tw_load_trace(path.encode(), None, 0, ctypes.byref(n)))
+    arr = (Request * max(n.value, 1))()
+    _wcheck(_S.tw_load_trace(path.encode(), arr, n.value, ctypes.byref(n)))
+    return [(arr[i].prompt_tokens, arr[i].output_tokens, arr[i].arrival_s) for i in range(n.value)]
+
+
+def save_trace(requests, path: str) -> None:
+    _wcheck(_S.tw_save_trace(_requests(requests), len(requests), path.encode()))
+
+
+def form_batches(requests, chunk_size: int):
+    """weavesim::form_batches -> [(total_tokens, decode_token_count, kv_context, [(request_id, start, len)])]."""
+    reqs = _requests(requests)
+    nb, ns = c_int64(), c_int64()
+    st = _S.tw_form_batches(reqs, len(requests), chunk_size, None, 0, None, 0, ctypes.byref(nb), ctypes.byref(ns))
+    if st != 1:  # TW_ERR_DIMENSION = "arrays too small" (sizes reported)
+        _wcheck(st)
+    b = (IterationBatch * max(nb.value, 1))()
+    sl = (PrefillSlice * max(ns.value, 1))()
+    _wcheck(_S.tw_form_batches(reqs, len(requests), chunk_size, b, nb.value, sl, ns.value, ctypes.byref(nb),
+                               ctypes.byref(ns)))
+    out = []
+    for k in range(nb.value):
+        x = b[k]
+        slices = [(sl[j].request_id, sl[j].start, sl[j].len) for j in range(x.first_slice, x.first_slice + x.num_slices)]
+        out.append((x.total_tokens, x.decode_token_count, x.kv_context, slices))
+    return out
 
 
 def make_split_plan(T: int, num_sms: int = 148, tile_tokens: int = 128, cta_columns: int = 32,
@@ -108,6 +189,13 @@ def _weave_lib():
     lib.tw_weave_run_ex.argtypes = [c_void_p, c_int64, c_int64, c_int, c_int, c_int, c_int, ctypes.c_uint,
                                     POINTER(c_float)]
     lib.tw_weave_run_ex.restype = c_int
+    lib.tw_weave_run_batch.argtypes = [c_void_p, c_int64, c_int64, c_int64, c_int, c_int, c_int, c_int,
+                                       ctypes.c_uint, POINTER(c_float)]
+    lib.tw_weave_run_batch.restype = c_int
+    lib.tw_weave_throughput.argtypes = [c_void_p, POINTER(Request), c_int64, c_int64, c_int, c_int64, c_int, c_int,
+                                        c_int, c_int, ctypes.c_uint, POINTER(ThroughputResult), POINTER(c_double),
+                                        c_int64]
+    lib.tw_weave_throughput.restype = c_int
     lib.tw_weave_trace.argtypes = [c_void_p, c_int, POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_int),
                                    POINTER(c_float), POINTER(c_float)]
     for f in ("tw_weave_create", "tw_weave_destroy", "tw_weave_run", "tw_weave_trace"):
@@ -154,6 +242,31 @@ class LayerRunner:
         check(self._L.tw_weave_run_ex(self._h, T, prefix, MODES[mode], boundary_sms, gemm_sms, layers,
                                       1 if graph else 0, ctypes.byref(us)))
         return us.value
+
+    def run_batch(self, T: int, kv_context: int, mode: str, prefix: int = 0, boundary_sms: int = 16,
+                  gemm_sms: int = 0, layers: int = 4, graph: bool = False) -> float:
+        """run() for one serving batch with kv_context prior-context tokens attended."""
+        us = c_float()
+        check(self._L.tw_weave_run_batch(self._h, T, prefix, kv_context, MODES[mode], boundary_sms, gemm_sms, layers,
+                                         1 if graph else 0, ctypes.byref(us)))
+        return us.value
+
+    def throughput(self, requests, chunk_size: int, mode: str, num_layers: int = 80, layers_measured: int = 2,
+                   boundary_sms: int = 16, gemm_sms: int = 0, graph: bool = False, threshold: int | None = None):
+        """Measured serving throughput over form_batches(requests, chunk_size)
+        (tw_weave_throughput): a ThroughputResult dict with per-iteration latencies."""
+        reqs = _requests(requests)
+        n_iter = len(form_batches(requests, chunk_size))
+        lat = (c_double * max(n_iter, 1))()
+        res = ThroughputResult()
+        check(self._L.tw_weave_throughput(self._h, reqs, len(requests), chunk_size, MODES[mode],
+                                          self.threshold if threshold is None else threshold, num_layers,
+                                          layers_measured, boundary_sms, gemm_sms, 1 if graph else 0,
+                                          ctypes.byref(res), lat, n_iter))
+        return {"tokens_per_sec": res.tokens_per_sec, "iterations": res.iterations,
+                "total_tokens": res.total_tokens, "total_seconds": res.total_seconds,
+                "mean_iteration_latency": res.mean_iteration_latency,
+                "iteration_latencies": [lat[i] for i in range(min(n_iter, res.iterations))]}
 
     def trace(self, max_events: int = 64):
         n = c_int()

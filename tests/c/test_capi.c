@@ -8,6 +8,7 @@
 #include "tw/tw.h"
 #include "tw/tw_split.h"
 #include "tw/tw_weave.h"
+#include "tw/tw_workload.h"
 
 static int failures = 0;
 #define EXPECT(c)                                              \
@@ -40,6 +41,21 @@ int main(void) {
     EXPECT(tw_make_split_plan(4096, 148, 128, 32, 1024, &a, &b, &off, &mode) == TW_OK);
     EXPECT(a == 1152 && b == 2944 && off == -896 && mode == 2);
     EXPECT(tw_make_split_plan(512, 148, 128, 32, 1024, &a, &b, &off, &mode) == TW_OK && mode == 1);
+  }
+  /* batch formation (proj/tests/test_workloads.cpp:108-119) */
+  {
+    tw_request req[1];
+    tw_iteration_batch b[8];
+    tw_prefill_slice sl[8];
+    int64_t nb = 0, ns = 0;
+    EXPECT(tw_synth_trace(1, 300, 3, req) == TW_OK);
+    EXPECT(tw_form_batches(req, 1, 100, b, 2, sl, 8, &nb, &ns) == TW_ERR_DIMENSION && nb == 6 && ns == 3);
+    EXPECT(tw_form_batches(req, 1, 100, b, 8, sl, 8, &nb, &ns) == TW_OK && nb == 6);
+    EXPECT(b[0].kv_context == 0 && b[3].kv_context == 300 && b[5].kv_context == 302 && b[5].num_slices == 0);
+    EXPECT(sl[2].start == 200 && sl[2].len == 100);
+    EXPECT(tw_form_batches(req, 1, 0, b, 8, sl, 8, &nb, &ns) == TW_ERR_CONFIG);
+    EXPECT(tw_load_trace("/nonexistent/trace.jsonl", NULL, 0, &nb) == TW_ERR_PARSE);
+    EXPECT(strstr(tw_workload_last_error(), "cannot open") != NULL);
   }
   printf("c-abi: %s (%d failures)\n", failures ? "FAIL" : "ok", failures);
   return failures ? 1 : 0;

@@ -8,6 +8,7 @@
 // Cases follow proj/tests/test_numerics.cpp, test_collectives.cpp,
 // test_splitter.cpp and acceptance.cpp check 1 (cited per case).
 #include <chrono>
+#include <fstream>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -18,6 +19,7 @@
 #include "weavesim/errors.hpp"
 #include "weavesim/numerics.hpp"
 #include "weavesim/splitter.hpp"
+#include "weavesim/workloads.hpp"
 
 using namespace weavesim;
 
@@ -268,12 +270,105 @@ void acceptance_cases(bool full) {
   if (full) CHECK(secs < 60.0);
 }
 
+// proj/tests/test_workloads.cpp:14-125, restated (host only).
+void workload_cases() {
+  {  // :14-26 trace JSONL round trip
+    const std::string path = "test_trace_roundtrip.jsonl";
+    std::vector<Request> requests = {{0, 100, 10, 0.0}, {1, 2048, 128, 0.5}, {2, 1, 0, 1.25}};
+    save_trace(requests, path);
+    const std::vector<Request> loaded = load_trace(path);
+    CHECK(loaded.size() == 3);
+    for (size_t i = 0; i < 3 && i < loaded.size(); ++i) {
+      CHECK(loaded[i].prompt_tokens == requests[i].prompt_tokens);
+      CHECK(loaded[i].output_tokens == requests[i].output_tokens);
+      CHECK(loaded[i].arrival_s == requests[i].arrival_s);
+    }
+    std::remove(path.c_str());
+  }
+  {  // :28-54 parse errors name the line
+    const std::string path = "test_trace_bad.jsonl";
+    {
+      std::ofstream out(path);
+      out << R"({"prompt_tokens": 10, "output_tokens": 2})" << "\n";
+      out << "not json\n";
+    }
+    bool named = false;
+    try {
+      load_trace(path);
+    } catch (const ParseError& e) {
+      named = std::string(e.what()).find("line 2") != std::string::npos;
+    }
+    CHECK(named);
+    {
+      std::ofstream out(path);
+      out << R"({"prompt_tokens": 10})" << "\n";
+    }
+    CHECK_THROWS_AS(load_trace(path), ParseError);
+    {
+      std::ofstream out(path);
+      out << R"({"prompt_tokens": 0, "output_tokens": 2})" << "\n";
+    }
+    CHECK_THROWS_AS(load_trace(path), ParseError);
+    std::remove(path.c_str());
+    CHECK_THROWS_AS(load_trace("missing_trace.jsonl"), ParseError);
+  }
+  {  // :56-70 conservation
+    std::int64_t prefill = 0, decode = 0;
+    for (const IterationBatch& b : form_batches(synth_trace(16, 1000, 37), 512)) {
+      std::int64_t slice_sum = 0;
+      for (const PrefillSlice& s : b.prefill_token_slices) slice_sum += s.len;
+      CHECK(b.total_tokens == slice_sum + b.decode_token_count);
+      prefill += slice_sum;
+      decode += b.decode_token_count;
+    }
+    CHECK(prefill == 16 * 1000);
+    CHECK(decode == 16 * 37);
+  }
+  {  // :72-80 budget
+    bool ok = true;
+    for (const IterationBatch& b : form_batches(synth_trace(8, 4096, 64), 1024)) {
+      std::int64_t slice_sum = 0;
+      for (const PrefillSlice& s : b.prefill_token_slices) slice_sum += s.len;
+      ok = ok && slice_sum <= 1024 && b.total_tokens <= 1024 + b.decode_token_count;
+    }
+    CHECK(ok);
+  }
+  {  // :82-98 FCFS, decode-only tail
+    const std::vector<IterationBatch> b = form_batches(synth_trace(4, 100, 5), 250);
+    CHECK(!b.empty() && b[0].prefill_token_slices.size() == 3);
+    if (!b.empty() && b[0].prefill_token_slices.size() == 3) {
+      CHECK(b[0].prefill_token_slices[0].request_id == 0);
+      CHECK(b[0].prefill_token_slices[2].request_id == 2);
+      CHECK(b[0].prefill_token_slices[2].len == 50);
+      CHECK(b[0].decode_token_count == 0);
+      CHECK(b[1].decode_token_count == 2);
+      CHECK(b.back().decode_only());
+    }
+  }
+  {  // :100-106 arrival ties
+    const std::vector<IterationBatch> b = form_batches({{0, 100, 0, 2.0}, {1, 100, 0, 0.0}, {2, 100, 0, 2.0}}, 100);
+    CHECK(b.size() == 3 && b[0].prefill_token_slices[0].request_id == 1 &&
+          b[1].prefill_token_slices[0].request_id == 0 && b[2].prefill_token_slices[0].request_id == 2);
+  }
+  {  // :108-119 kv context
+    const std::vector<IterationBatch> b = form_batches(synth_trace(1, 300, 3), 100);
+    CHECK(b.size() == 6);
+    const std::int64_t want[6] = {0, 100, 200, 300, 301, 302};
+    for (size_t i = 0; i < 6 && i < b.size(); ++i) CHECK(b[i].kv_context == want[i]);
+  }
+  // :121-125 bad arguments
+  CHECK_THROWS_AS(form_batches({}, 0), ConfigError);
+  CHECK_THROWS_AS(synth_trace(0, 100, 10), ConfigError);
+  CHECK_THROWS_AS(synth_trace(4, 0, 10), ConfigError);
+}
+
 }  // namespace
 
 // usage: test_dropin host | gpu | acceptance
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "host";
   host_cases();
+  workload_cases();
   if (mode == "gpu") {
     gpu_cases();
     acceptance_cases(false);

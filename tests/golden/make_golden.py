@@ -47,6 +47,42 @@ PLAN_CASES = [("b200", "llama-70b", t) for t in (256, 512, 1024, 2048, 4096, 614
              [("h100", "llama-70b", t) for t in (1024, 2048, 4096, 8192, 16384)]
 
 
+
+def synth(count, prompt, output):
+    """synth_trace (proj/src/workloads.cpp:56-66) as (prompt, output, arrival) tuples."""
+    return [(prompt, output, 0.0)] * count
+
+
+def mixed_trace(seed: int, n: int, max_prompt: int, max_output: int):
+    """Portable mixed-length trace with arrival-time ties (numpy PCG64)."""
+    rng = np.random.default_rng(seed)
+    return [(int(rng.integers(1, max_prompt + 1)), int(rng.integers(0, max_output + 1)),
+             float(rng.choice([0.0, 0.25, 0.5, 1.0]))) for _ in range(n)]
+
+
+# form_batches cases: proj/tests/test_workloads.cpp:56-132 plus mixed traces.
+BATCH_CASES = [
+    ("conservation", synth(16, 1000, 37), 512),        # test_workloads.cpp:56-70
+    ("budget", synth(8, 4096, 64), 1024),               # :72-80
+    ("fcfs", synth(4, 100, 5), 250),                    # :82-98
+    ("arrival_ties", [(100, 0, 2.0), (100, 0, 0.0), (100, 0, 2.0)], 100),  # :100-106
+    ("kv_context", synth(1, 300, 3), 100),              # :108-119
+    ("decode_over_budget", synth(12, 50, 40), 8),
+    ("no_output", [(7, 0, 0.0), (3, 0, 0.0)], 4),
+    ("empty", [], 16),
+    ("mixed_a", mixed_trace(11, 40, 3000, 200), 2048),
+    ("mixed_b", mixed_trace(12, 64, 700, 50), 333),
+    ("mixed_c", mixed_trace(13, 25, 9000, 16), 8192),
+]
+
+# Serving workloads of tools/throughput_bench.py: (name, model, requests, chunk).
+THROUGHPUT_CASES = [
+    ("llama-70b", "llama-70b", synth(32, 2048, 128), 8192),
+    ("llama-70b-chunk4k", "llama-70b", synth(32, 2048, 128), 4096),
+    ("mixtral-8x22b", "mixtral-8x22b", synth(32, 2048, 128), 8192),
+]
+
+
 def main() -> None:
     ref = oracle.RefLib()
     arrays = {}
@@ -81,6 +117,25 @@ def main() -> None:
             for mode in ("multimem", "fuseonly", "tokenweave", "nocomm"):
                 row[mode] = ref.layer_latency("b200", model, t, mode)
             meta["layer_latency_s"].append(row)
+    meta["batches"] = []
+    for name, reqs, chunk in BATCH_CASES:
+        meta["batches"].append({"name": name, "requests": [list(r) for r in reqs], "chunk_size": chunk,
+                                "batches": [[t, d, kv, [list(x) for x in sl]]
+                                            for t, d, kv, sl in ref.form_batches(reqs, chunk)]})
+    # save_trace text of the reference (byte-exact drop-in check).
+    import tempfile
+    trace = [(100, 10, 0.0), (2048, 128, 0.5), (1, 0, 1.25), (5, 3, 1e-7), (9, 9, 3.0), (4, 1, 123456.789)]
+    with tempfile.TemporaryDirectory() as d:
+        path = os.path.join(d, "t.jsonl")
+        ref.save_trace(trace, path)
+        meta["trace_text"] = {"requests": [list(r) for r in trace], "text": open(path).read()}
+    meta["throughput_pred"] = []
+    for name, model, reqs, chunk in THROUGHPUT_CASES:
+        row = {"name": name, "model": model, "count": len(reqs), "prompt": reqs[0][0], "output": reqs[0][1],
+               "chunk_size": chunk}
+        for mode in ("multimem", "fuseonly", "tokenweave", "nocomm"):
+            row[mode] = ref.simulate_throughput("b200", model, mode, reqs, chunk)
+        meta["throughput_pred"].append(row)
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=1)

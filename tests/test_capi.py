@@ -30,6 +30,19 @@ def test_library_exports_every_declared_symbol():
     assert sorted(L.exported_symbols()) == declared_symbols()
 
 
+@pytest.mark.parametrize("header,lib", [("tw_split.h", "libweavesim_b200.so"),
+                                        ("tw_workload.h", "libweavesim_b200.so"),
+                                        ("tw_weave.h", "libtw_weave.so")])
+def test_layer_libraries_export_their_headers(header, lib):
+    with open(os.path.join(ROOT, "include", "tw", header)) as f:
+        syms = set(re.findall(r"^TW_API\s+[\w\s\*]+?\b(tw_\w+)\s*\(", f.read(), flags=re.M))
+    assert syms
+    import paper_2505_11329_b200._lib  # noqa: F401  (libtw.so first, as a host would)
+    so = ctypes.CDLL(os.path.join(ROOT, "paper_2505_11329_b200", "lib", lib))
+    for s in sorted(syms):
+        assert hasattr(so, s), f"{lib} does not export {s}"
+
+
 def test_version_and_abi():
     import paper_2505_11329_b200 as tw
     from paper_2505_11329_b200 import _lib
