@@ -53,6 +53,9 @@ typedef enum tw_weave_op { TW_OP_ATTENTION = 0, TW_OP_FFN = 1, TW_OP_FUSED = 2 }
 
 typedef struct tw_weave* tw_weave_t;
 
+/* Message of the last failing call of this header on this thread ("" if none). */
+TW_API const char* tw_weave_last_error(void);
+
 TW_API tw_status tw_weave_create(const tw_layer_spec* spec, int64_t max_tokens, int device, tw_weave_t* out);
 /* TP >= 2 with one process per GPU: `comm` is a multi-process communicator
  * (tw_comm_create_mp, buffers >= max_tokens*hidden*2 B) and spec->tp its world

@@ -325,6 +325,8 @@ tw_status unfused(tw_weave* w, int64_t r0, int64_t n, cudaStream_t s) {
 
 extern "C" {
 
+const char* tw_weave_last_error(void) { return g_err; }
+
 static tw_status weave_create(const tw_layer_spec* spec, int64_t max_tokens, int device, tw_comm_t comm,
                               tw_weave_t* out);
 

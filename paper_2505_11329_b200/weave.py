@@ -196,6 +196,8 @@ def _weave_lib():
                                         c_int, c_int, ctypes.c_uint, POINTER(ThroughputResult), POINTER(c_double),
                                         c_int64]
     lib.tw_weave_throughput.restype = c_int
+    lib.tw_weave_last_error.restype = ctypes.c_char_p
+    lib.tw_weave_last_error.argtypes = []
     lib.tw_weave_trace.argtypes = [c_void_p, c_int, POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_int),
                                    POINTER(c_float), POINTER(c_float)]
     for f in ("tw_weave_create", "tw_weave_destroy", "tw_weave_run", "tw_weave_trace"):
@@ -218,10 +220,13 @@ class LayerRunner:
         self.model = model
         h = c_void_p()
         if comm is not None:
-            check(self._L.tw_weave_create_tp(ctypes.byref(self.spec), max_tokens, comm, ctypes.byref(h)))
+            self._check(self._L.tw_weave_create_tp(ctypes.byref(self.spec), max_tokens, comm, ctypes.byref(h)))
         else:
-            check(self._L.tw_weave_create(ctypes.byref(self.spec), max_tokens, device, ctypes.byref(h)))
+            self._check(self._L.tw_weave_create(ctypes.byref(self.spec), max_tokens, device, ctypes.byref(h)))
         self._h = h
+
+    def _check(self, status: int) -> None:
+        check(status, self._L.tw_weave_last_error)
 
     def close(self):
         if self._h:
@@ -239,7 +244,7 @@ class LayerRunner:
         """Device time per layer (us).  graph=True: the layers are captured in
         one CUDA graph and the replay is timed (no per-op trace)."""
         us = c_float()
-        check(self._L.tw_weave_run_ex(self._h, T, prefix, MODES[mode], boundary_sms, gemm_sms, layers,
+        self._check(self._L.tw_weave_run_ex(self._h, T, prefix, MODES[mode], boundary_sms, gemm_sms, layers,
                                       1 if graph else 0, ctypes.byref(us)))
         return us.value
 
@@ -247,7 +252,7 @@ class LayerRunner:
                   gemm_sms: int = 0, layers: int = 4, graph: bool = False) -> float:
         """run() for one serving batch with kv_context prior-context tokens attended."""
         us = c_float()
-        check(self._L.tw_weave_run_batch(self._h, T, prefix, kv_context, MODES[mode], boundary_sms, gemm_sms, layers,
+        self._check(self._L.tw_weave_run_batch(self._h, T, prefix, kv_context, MODES[mode], boundary_sms, gemm_sms, layers,
                                          1 if graph else 0, ctypes.byref(us)))
         return us.value
 
@@ -259,7 +264,7 @@ class LayerRunner:
         n_iter = len(form_batches(requests, chunk_size))
         lat = (c_double * max(n_iter, 1))()
         res = ThroughputResult()
-        check(self._L.tw_weave_throughput(self._h, reqs, len(requests), chunk_size, MODES[mode],
+        self._check(self._L.tw_weave_throughput(self._h, reqs, len(requests), chunk_size, MODES[mode],
                                           self.threshold if threshold is None else threshold, num_layers,
                                           layers_measured, boundary_sms, gemm_sms, 1 if graph else 0,
                                           ctypes.byref(res), lat, n_iter))
@@ -272,6 +277,6 @@ class LayerRunner:
         n = c_int()
         op, sp, st = (c_int * max_events)(), (c_int * max_events)(), (c_int * max_events)()
         a, b = (c_float * max_events)(), (c_float * max_events)()
-        check(self._L.tw_weave_trace(self._h, max_events, ctypes.byref(n), op, sp, st, a, b))
+        self._check(self._L.tw_weave_trace(self._h, max_events, ctypes.byref(n), op, sp, st, a, b))
         return [{"op": OPS[op[i]], "split": SPLITS[sp[i]], "stream": "comm" if st[i] else "compute",
                  "start_us": a[i], "end_us": b[i]} for i in range(n.value)]

@@ -96,6 +96,12 @@ WEAVE_WORKER = textwrap.dedent("""
     dist.barrier()
     # K1 inside a CUDA graph, replayed: barrier generations live on the device
     out["tokenweave_graph"] = r.run(T, "tokenweave", prefix=320, boundary_sms=4, layers=2, graph=True)
+    # measured serving throughput in TP mode: chunked-prefill batches (with
+    # prior-context attention) through K1, identical call sequence per rank
+    dist.barrier()
+    tp = r.throughput(weave.synth_trace(3, 200, 4), 256, "tokenweave", num_layers=2, layers_measured=1,
+                      boundary_sms=4, threshold=256)
+    out["throughput"] = {{k: tp[k] for k in ("iterations", "total_tokens", "tokens_per_sec")}}
     _lib.check(_lib.lib.tw_comm_check(h))
     print(json.dumps(out), flush=True)
     dist.barrier()
@@ -128,6 +134,9 @@ def test_weave_tp_runner_two_processes(cuda, tmp_path):
         assert len(res["fuseonly_ops"]) == 4 and len(res["unfused_ops"]) == 4
         ops = res["tokenweave_ops"]
         assert len(ops) == 8 and sum(1 for op, _, st in ops if op == "fused_ar_norm" and st == "comm") == 4
+        assert res["throughput"]["total_tokens"] == 3 * (200 + 4) and res["throughput"]["tokens_per_sec"] > 0
+        from paper_2505_11329_b200 import weave
+        assert res["throughput"]["iterations"] == len(weave.form_batches(weave.synth_trace(3, 200, 4), 256))
 
 
 def test_two_processes_one_gpu_peer_fallback(cuda, orc, tmp_path):
