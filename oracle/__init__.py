@@ -189,6 +189,9 @@ class RefLib:
         L.ref_save_trace.argtypes = [_I64, _D, c_int64, c_char_p]
         L.ref_load_trace.argtypes = [c_char_p, _I64, _D, c_int64, _I64]
         L.ref_simulate_throughput.argtypes = [c_char_p, c_char_p, c_char_p, _I64, c_int64, c_int64, _D]
+        L.ref_cmd_throughput_csv.argtypes = [c_char_p, c_char_p, c_int64, c_uint64, c_char_p, c_int64]
+        L.ref_cmd_throughput_csv.restype = c_int64
+        L.ref_chatlike_trace.argtypes = [c_int64, c_uint64, _I64]
         self.L = L
 
     def rmsnorm_residual(self, inp, res, weight, eps=1e-5):
@@ -342,6 +345,22 @@ class RefLib:
             raise StatusError(st, "ref_simulate_throughput")
         return {"tokens_per_sec": out[0], "iterations": int(out[1]), "total_tokens": int(out[2]),
                 "total_seconds": out[3]}
+
+    def cmd_throughput_csv(self, model="llama-70b", profile="b200", chunk=2048, seed=42) -> str:
+        """The reference CLI `weavesim throughput` CSV, run as shipped."""
+        n = self.L.ref_cmd_throughput_csv(model.encode(), profile.encode(), chunk, seed, None, 0)
+        if n < 0:
+            raise StatusError(9, "ref_cmd_throughput_csv")
+        buf = ctypes.create_string_buffer(n + 1)
+        self.L.ref_cmd_throughput_csv(model.encode(), profile.encode(), chunk, seed, buf, n + 1)
+        return buf.value.decode()
+
+    def chatlike_trace(self, count=96, seed=42):
+        out = (c_int64 * (2 * count))()
+        st = self.L.ref_chatlike_trace(count, seed, out)
+        if st:
+            raise StatusError(st, "ref_chatlike_trace")
+        return [(out[2 * i], out[2 * i + 1], 0.0) for i in range(count)]
 
 
 def _unpack_batches(out4, sl3, nb):

@@ -8,6 +8,7 @@
 // DimensionError 1, NumericError 2, ConfigError 3, ContractError 4, other 9.
 #include <algorithm>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <random>
@@ -15,6 +16,7 @@
 #include <vector>
 
 #include "weavesim/calibration.hpp"
+#include "weavesim/commands.hpp"
 #include "weavesim/collectives.hpp"
 #include "weavesim/errors.hpp"
 #include "weavesim/numerics.hpp"
@@ -380,6 +382,45 @@ int ref_simulate_throughput(const char* profile, const char* model, const char* 
     out4[1] = static_cast<double>(r.iterations);
     out4[2] = static_cast<double>(r.total_tokens);
     out4[3] = r.total_seconds;
+  });
+}
+
+// The reference CLI's `throughput` command (proj/src/commands.cpp:432-480),
+// run as shipped: its CSV (modeled tokens/s of the fixed-2048x128 and
+// chatlike traces, every mode) into buf.  Returns the CSV length.
+long long ref_cmd_throughput_csv(const char* model, const char* profile, std::int64_t chunk, std::uint64_t seed,
+                                 char* buf, long long cap) {
+  long long n = -1;
+  guarded([&] {
+    RunConfig c;
+    c.model = model;
+    c.profile = profile;
+    c.chunk_size = chunk;
+    c.seed = seed;
+    const CommandResult r = cmd_throughput(c);
+    n = static_cast<long long>(r.csv.size());
+    if (buf && cap > 0) {
+      const long long m = std::min<long long>(n, cap - 1);
+      std::memcpy(buf, r.csv.data(), static_cast<size_t>(m));
+      buf[m] = '\0';
+    }
+  });
+  return n;
+}
+
+// Restatement of the CLI's chatlike_trace (proj/src/commands.cpp:59-75,
+// anonymous there): lognormal prompts / replies from std::mt19937_64(seed),
+// clamped.  Test infrastructure: pinned by feeding it to simulate_throughput
+// and matching ref_cmd_throughput_csv's chatlike rows.  out2 = {prompt, output}.
+int ref_chatlike_trace(std::int64_t count, std::uint64_t seed, std::int64_t* out2) {
+  return guarded([&] {
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> prompt_log(6.8, 0.9);
+    std::normal_distribution<double> output_log(4.0, 0.7);
+    for (std::int64_t i = 0; i < count; ++i) {
+      out2[2 * i] = std::clamp<std::int64_t>(std::llround(std::exp(prompt_log(rng))), 32, 8192);
+      out2[2 * i + 1] = std::clamp<std::int64_t>(std::llround(std::exp(output_log(rng))), 16, 256);
+    }
   });
 }
 

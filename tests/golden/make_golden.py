@@ -76,11 +76,19 @@ BATCH_CASES = [
 ]
 
 # Serving workloads of tools/throughput_bench.py: (name, model, requests, chunk).
-THROUGHPUT_CASES = [
-    ("llama-70b", "llama-70b", synth(32, 2048, 128), 8192),
-    ("llama-70b-chunk4k", "llama-70b", synth(32, 2048, 128), 4096),
-    ("mixtral-8x22b", "mixtral-8x22b", synth(32, 2048, 128), 8192),
-]
+# The first two are the reference CLI's own `throughput` defaults
+# (proj/src/commands.cpp:432-446: synth_trace(64, 2048, 128) and
+# chatlike_trace(96, seed 42), chunk 2048 = RunConfig's default); chatlike
+# requests come from the reference (restated in oracle/ref_capi.cpp, pinned
+# against the CLI's CSV), so they are stored in the fixture.
+def throughput_cases(ref):
+    chat = ref.chatlike_trace(96, 42)
+    return [
+        ("fixed-2048x128", "llama-70b", synth(64, 2048, 128), 2048),
+        ("chatlike", "llama-70b", chat, 2048),
+        ("fixed-2048x128-chunk8192", "llama-70b", synth(64, 2048, 128), 8192),
+        ("mixtral-fixed-2048x128-chunk8192", "mixtral-8x22b", synth(64, 2048, 128), 8192),
+    ]
 
 
 def main() -> None:
@@ -130,12 +138,12 @@ def main() -> None:
         ref.save_trace(trace, path)
         meta["trace_text"] = {"requests": [list(r) for r in trace], "text": open(path).read()}
     meta["throughput_pred"] = []
-    for name, model, reqs, chunk in THROUGHPUT_CASES:
-        row = {"name": name, "model": model, "count": len(reqs), "prompt": reqs[0][0], "output": reqs[0][1],
-               "chunk_size": chunk}
-        for mode in ("multimem", "fuseonly", "tokenweave", "nocomm"):
+    for name, model, reqs, chunk in throughput_cases(ref):
+        row = {"name": name, "model": model, "chunk_size": chunk, "requests": [[p, o] for p, o, _ in reqs]}
+        for mode in ("default", "multimem", "fuseonly", "tokenweave", "nocomm"):
             row[mode] = ref.simulate_throughput("b200", model, mode, reqs, chunk)
         meta["throughput_pred"].append(row)
+    meta["cli_throughput_csv"] = ref.cmd_throughput_csv("llama-70b", "b200", 2048, 42)
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=1)

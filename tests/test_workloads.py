@@ -159,8 +159,24 @@ def test_throughput_predictions_fixture(golden):
     meta, _ = golden
     for row in meta["throughput_pred"]:
         assert row["nocomm"]["tokens_per_sec"] >= row["multimem"]["tokens_per_sec"]
-        n = len(weave.form_batches(weave.synth_trace(row["count"], row["prompt"], row["output"]), row["chunk_size"]))
-        assert row["tokenweave"]["iterations"] == n
+        reqs = [(p, o, 0.0) for p, o in row["requests"]]
+        assert row["tokenweave"]["iterations"] == len(weave.form_batches(reqs, row["chunk_size"]))
+        assert row["tokenweave"]["total_tokens"] == sum(p + o for p, o in row["requests"])
+
+
+def test_cli_throughput_workloads_pinned(golden, ref):
+    """The fixture's fixed-2048x128 / chatlike requests are the ones the
+    reference CLI's `throughput` command simulates (proj/src/commands.cpp:
+    432-480): the reference's own CSV, re-derived from the fixture rows."""
+    meta, _ = golden
+    csv = ref.cmd_throughput_csv("llama-70b", "b200", 2048, 42)
+    assert csv == meta["cli_throughput_csv"]
+    rows = {(ln.split(",")[0], ln.split(",")[1]): ln.split(",") for ln in csv.strip().splitlines()[1:]}
+    for case in meta["throughput_pred"][:2]:
+        for mode in ("default", "multimem", "nocomm", "fuseonly", "tokenweave"):
+            got = case[mode]
+            want = rows[(case["name"], mode)]
+            assert f"{got['tokens_per_sec']:.2f}" == want[2] and got["iterations"] == int(want[3])
 
 
 @pytest.mark.gpu

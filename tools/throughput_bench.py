@@ -3,7 +3,10 @@
 two-stream runner (tw_weave_throughput), per mode -- the reference's
 simulate_throughput (:111-141) with every iteration MEASURED instead of priced.
 
-Per workload (tests/golden/make_golden.py THROUGHPUT_CASES): tokens/s of the
+Workloads (tests/golden/make_golden.py throughput_cases): the reference CLI's
+own `throughput` defaults -- fixed-2048x128 (64 requests) and chatlike (96
+lognormal requests, seed 42) at chunk 2048 (proj/src/commands.cpp:432-446) --
+plus chunk-8192 variants for Llama and Mixtral.  Per workload: tokens/s of the
 unfused sequential layer, fuse-only, TokenWeave (decode-only and
 below-threshold batches run fuse-only, scheduler.cpp:333-341) and the no-comm
 bound, each iteration = measured per-layer time x num_layers (80 for
@@ -25,6 +28,8 @@ sys.path.insert(0, ROOT)
 
 NUM_LAYERS = {"llama-70b": 80, "qwen-72b": 80, "mixtral-8x22b": 56}  # proj/src/presets.cpp:72-97
 MODES = ("unfused", "fuseonly", "tokenweave", "nocomm")
+# measured mode -> the reference BaselineMode it is compared with (Multimem =
+# the unfused sequential layer with the best AllReduce, scheduler.cpp:153-164)
 PRED_MODE = {"unfused": "multimem", "fuseonly": "fuseonly", "tokenweave": "tokenweave", "nocomm": "nocomm"}
 
 
@@ -71,7 +76,7 @@ def main():
            "rows": []}
     for case in cases:
         model = case["model"]
-        reqs = weave.synth_trace(case["count"], case["prompt"], case["output"])
+        reqs = [(p, o, 0.0) for p, o in case["requests"]]
         batches = weave.form_batches(reqs, case["chunk_size"])
         max_t = max(b[0] for b in batches)
         kw = {}
@@ -83,8 +88,9 @@ def main():
             comm = h
             kw["comm"] = h
         r = weave.LayerRunner(model, tp=tp, max_tokens=max_t, **kw)
-        row = {"name": case["name"], "model": model, "requests": case["count"], "prompt": case["prompt"],
-               "output": case["output"], "chunk_size": case["chunk_size"], "iterations": len(batches),
+        row = {"name": case["name"], "model": model, "requests": len(reqs),
+               "prompt_tokens": sum(p for p, _, _ in reqs), "output_tokens": sum(o for _, o, _ in reqs),
+               "chunk_size": case["chunk_size"], "iterations": len(batches),
                "num_layers": NUM_LAYERS[model],
                "overlap_batches": sum(1 for b in batches if b[3] and weave.make_split_plan(
                    b[0], threshold=r.threshold)[3] == 2)}
