@@ -349,7 +349,7 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
     f.H = H;
     f.V = static_cast<int>(H / nv);
     f.eps = eps;
-    cudaError_t e = launch_k2_flat(f, bf16, sms, static_cast<cudaStream_t>(stream));
+    cudaError_t e = launch_k2_flat(f, bf16, sms, sm_budget > 0, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "rmsnorm_residual (flat) launch");
     return TW_OK;
   }
@@ -382,6 +382,11 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
       q.H = H;
       q.V = bp.V;
       q.tpr = bp.tpr;
+      // Consumer row groups per CTA (k2_tma_kernel): TW_K2_GROUPS overrides.
+      static const char* groups_env = std::getenv("TW_K2_GROUPS");
+      q.groups = 1;
+      if (groups_env) q.groups = std::max(1, std::min(2, std::atoi(groups_env)));
+      if (q.groups * bp.tpr > kBulkMaxConsumers) q.groups = 1;
       q.stages = stages;
       q.row_bytes = row_bytes;
       q.eps = eps;
@@ -398,7 +403,8 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
     return fail(TW_ERR_DIMENSION, "rmsnorm_residual: hidden size too large for the row engine");
   static const char* pipe_env = std::getenv("TW_ROWS_PIPELINE");
   plan.pipeline = pipe_env && pipe_env[0] == '1';
-  const int bpsm = std::max(1, rownorm_blocks_per_sm(plan, bf16, Xport::Local));
+  // An explicit budget is SMs: one CTA each (more CTAs would spread over more SMs).
+  const int bpsm = sm_budget > 0 ? 1 : std::max(1, rownorm_blocks_per_sm(plan, bf16, Xport::Local));
   const long long need = (T + plan.groups - 1) / plan.groups;
   const int grid = static_cast<int>(std::min<long long>(need, static_cast<long long>(sms) * bpsm));
   RowParams p = {};

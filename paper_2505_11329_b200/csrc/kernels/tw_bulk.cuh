@@ -76,7 +76,8 @@ struct BulkParams {
   const float* weight;
   long long T, H;
   int V;       // 16-byte vectors per row
-  int tpr;     // consumer threads (multiple of 32)
+  int tpr;     // consumer threads per row group (multiple of 32)
+  int groups;  // k2_tma_kernel: consumer row groups per CTA (1 or 2; groups * tpr <= 512)
   int stages;  // smem ring depth
   uint32_t row_bytes;
   float eps;
@@ -225,15 +226,21 @@ __device__ __forceinline__ void sts_v4(void* p, uint4 v) {
 // store units only touch shared memory; HBM traffic is issued by TMA.
 template <class E, int VPT>
 __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const __grid_constant__ BulkParams p) {
+  // G consumer row groups: group g takes the CTA's rows i = g, g+G, ... (stage
+  // i % S), with its own named barrier, partial-sum slots and storer thread,
+  // so G rows are normalised concurrently per SM while the ring keeps up to S
+  // rows of loads in flight.  G = 2 roughly doubles what one SM moves when the
+  // SM count is budgeted (the weave's boundary op); one CTA per SM either way.
   constexpr int N = 16 / sizeof(E);
   using VT = Vec<E, N>;
   using Acc = typename std::conditional<sizeof(E) == 4, double, float>::type;
   extern __shared__ __align__(128) unsigned char smem[];
   const int S = p.stages;
+  const int G = p.groups;
   unsigned char* ring = smem;  // [S][2][row_bytes]: slot 0 input/output, slot 1 residual/r'
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(S) * 2 * p.row_bytes);
   uint64_t* empty = full + S;
-  Acc* part = reinterpret_cast<Acc*>(empty + S);
+  Acc* part = reinterpret_cast<Acc*>(empty + S);  // [G][2][consumer warps per group]
 
   const int tpr = p.tpr;
   const int cwarps = tpr >> 5;
@@ -242,7 +249,7 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);  // released by the storer only
+      mbar_init(&empty[s], 1);  // released by the storer of the row that used it
     }
     mbar_fence_init();
   }
@@ -266,8 +273,9 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     return;
   }
 
-  const int lt = threadIdx.x - 32;
-  const int cw = warp - 1;
+  const int grp = (threadIdx.x - 32) / tpr;
+  const int lt = threadIdx.x - 32 - grp * tpr;
+  const int cw = lt >> 5;
   const bool storer = lt == 0;
   float w[VPT][N];
 #pragma unroll
@@ -275,7 +283,9 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     const int c = lt + k * tpr;
     if (c < p.V) load_weight<N>(p.weight, static_cast<long long>(c) * N, w[k]);
   }
-  for (long long i = 0; i < nrows; ++i) {
+  long long prev = -1;  // this group's previous row index (its stage is released one row late)
+  int parity = 0;
+  for (long long i = grp; i < nrows; i += G, parity ^= 1) {
     const int s = static_cast<int>(i % S);
     const uint32_t ph = static_cast<uint32_t>((i / S) & 1);
     const long long row = blockIdx.x + i * gridDim.x;
@@ -301,9 +311,9 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     }
     ss = warp_sum(ss);
     Acc total;
-    Acc* pp = part + (i & 1) * cwarps;
+    Acc* pp = part + (grp * 2 + parity) * cwarps;
     if (lane == 0) pp[cw] = ss;
-    named_bar_sync(1, tpr);
+    named_bar_sync(1 + grp, tpr);
     total = 0;
     for (int q = 0; q < cwarps; ++q) total += pp[q];
     const float inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(p.H)) + p.eps);
@@ -319,21 +329,22 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
       }
     }
     fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk engine
-    named_bar_sync(1, tpr);
+    named_bar_sync(1 + grp, tpr);
     if (storer) {
       bulk_s2g(static_cast<unsigned char*>(p.out) + row * p.row_bytes, st, p.row_bytes);
       bulk_s2g(static_cast<unsigned char*>(p.res_out) + row * p.row_bytes, st + p.row_bytes, p.row_bytes);
       bulk_commit();
-      // the previous row's stores have finished reading their stage: free it
-      if (i > 0) {
+      // this storer's previous row's stores have finished reading their stage: free it
+      if (prev >= 0) {
         bulk_wait_read<1>();
-        mbar_arrive(&empty[(i - 1) % S]);
+        mbar_arrive(&empty[prev % S]);
       }
     }
+    prev = i;
   }
   if (storer) {
     bulk_wait_all();
-    if (nrows > 0) mbar_arrive(&empty[(nrows - 1) % S]);
+    if (prev >= 0) mbar_arrive(&empty[prev % S]);
   }
 }
 

@@ -162,26 +162,29 @@ BulkFn pick_bulk_e(int vpt, bool tma_store) {
 }
 }  // namespace
 
-size_t bulk_smem_bytes(int stages, uint32_t row_bytes, int tpr) {
-  return static_cast<size_t>(stages) * 2 * row_bytes + 2 * stages * sizeof(uint64_t) + 2 * (tpr / 32) * sizeof(double);
+size_t bulk_smem_bytes(int stages, uint32_t row_bytes, int tpr, int groups) {
+  return static_cast<size_t>(stages) * 2 * row_bytes + 2 * stages * sizeof(uint64_t) +
+         2 * static_cast<size_t>(std::max(groups, 1)) * (tpr / 32) * sizeof(double);
 }
 
 cudaError_t launch_k2_bulk(const BulkParams& params, int vpt, bool bf16, int grid, cudaStream_t stream,
                            bool tma_store) {
   BulkFn fn = bf16 ? pick_bulk_e<uint16_t>(vpt, tma_store) : pick_bulk_e<float>(vpt, tma_store);
   if (!fn) return cudaErrorInvalidConfiguration;
-  const size_t smem = bulk_smem_bytes(params.stages, params.row_bytes, params.tpr);
+  BulkParams p = params;
+  if (!tma_store || p.groups < 1) p.groups = 1;  // the register-store engine has one row group
+  const size_t smem = bulk_smem_bytes(p.stages, p.row_bytes, p.tpr, p.groups);
   cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  BulkParams p = params;
   void* args[] = {&p};
-  return cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(params.tpr + 32), args, smem, stream);
+  return cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(p.groups * p.tpr + 32), args, smem,
+                          stream);
 }
 
 // ---- K2 flat engine ----------------------------------------------------------------
 
-cudaError_t launch_k2_flat(const FlatParams& params, bool bf16, int sms, cudaStream_t stream) {
+cudaError_t launch_k2_flat(const FlatParams& params, bool bf16, int sms, bool one_cta_per_sm, cudaStream_t stream) {
   const int vpt_needed = (params.V + 1023) / 1024;
   using FlatFn = void (*)(FlatParams);
   FlatFn fn = nullptr;
@@ -198,6 +201,7 @@ cudaError_t launch_k2_flat(const FlatParams& params, bool bf16, int sms, cudaStr
   const int threads = std::max(32, ((params.V + vpt - 1) / vpt + 31) / 32 * 32);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn), threads, 0);
+  if (one_cta_per_sm) per_sm = 1;  // an explicit SM budget: more CTAs would spread over more SMs
   const long long grid = std::min<long long>(params.T, static_cast<long long>(sms) * std::max(per_sm, 1));
   FlatParams p = params;
   void* args[] = {&p};

@@ -28,11 +28,11 @@ cudaError_t launch_rownorm(const RowParams& params, const RowPlan& plan, bool bf
 cudaError_t launch_allreduce(const RowParams& params, const RowPlan& plan, bool bf16, Xport x, dim3 grid,
                              cudaStream_t stream);
 int rownorm_blocks_per_sm(const RowPlan& plan, bool bf16, Xport x);
-size_t bulk_smem_bytes(int stages, uint32_t row_bytes, int tpr);
+size_t bulk_smem_bytes(int stages, uint32_t row_bytes, int tpr, int groups);
 cudaError_t launch_k2_bulk(const BulkParams& params, int vpt, bool bf16, int grid, cudaStream_t stream,
                            bool tma_store);
 // K2 flat engine (tw_flat.cuh); V <= 2048 vectors per row.
-cudaError_t launch_k2_flat(const FlatParams& params, bool bf16, int sms, cudaStream_t stream);
+cudaError_t launch_k2_flat(const FlatParams& params, bool bf16, int sms, bool one_cta_per_sm, cudaStream_t stream);
 cudaError_t launch_count_nonfinite(const void* x, long long n, bool bf16, int* count, cudaStream_t stream);
 
 }  // namespace tw

@@ -92,17 +92,19 @@ def test_k2_host_buffers_pipeline(cuda, orc, T, H, chunk, pinned):
     assert_bf16_close(out.float().numpy(), want_out)
 
 
-@pytest.mark.parametrize("engine,pipeline", [("rows", "1"), ("rows", "0"), ("bulk", "0"), ("tma", "0"), ("flat", "0")])
-def test_k2_every_engine_matches_oracle(cuda, engine, pipeline):
+@pytest.mark.parametrize("engine,pipeline,groups", [("rows", "1", "1"), ("rows", "0", "1"), ("bulk", "0", "1"),
+                                                    ("tma", "0", "1"), ("tma", "0", "2"), ("flat", "0", "1")])
+def test_k2_every_engine_matches_oracle(cuda, engine, pipeline, groups):
     """Every K2 engine (and the software-pipelined row loop that the NVLS K1
     path uses) against the oracle: the parity tests above re-run in a
     subprocess with the engine forced (the selection is read once per process)."""
     import os
     import subprocess
     import sys
-    env = dict(os.environ, TW_K2_ENGINE=engine, TW_ROWS_PIPELINE=pipeline)
+    env = dict(os.environ, TW_K2_ENGINE=engine, TW_ROWS_PIPELINE=pipeline, TW_K2_GROUPS=groups)
     p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
-                        "matches_oracle and not every_engine or in_place or full_size or host_buffers"],
+                        "matches_oracle and not every_engine or in_place or full_size or host_buffers "
+                        "or sm_budget"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
     assert " passed" in p.stdout
