@@ -321,17 +321,17 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
   // rows, H % (16/elem) == 0).  TW_K2_ENGINE=rows forces the row engine.
   static const char* engine_env = std::getenv("TW_K2_ENGINE");
   // Default by row size (measured on B200, profiles/k2_engines_r01.txt): rows
-  // >= 16 KB -> TMA loads + TMA stores; 12-16 KB -> TMA loads + register
-  // stores; smaller rows -> the register row engine (per-row barrier and bulk
-  // issue costs dominate short rows).
+  // >= 12 KB -> the TMA engine (bulk loads + bulk stores); smaller rows -> the
+  // register row engine (per-row barrier and bulk issue costs dominate short
+  // rows).  The TMA engine with two consumer row groups beats the
+  // register-store variant at 12 KB rows (H = 6144 bf16: 30.8 vs 41.0 us at
+  // T = 4096, tools/k2_groups_ab.py), which is kept for A/B (TW_K2_ENGINE=bulk).
   const size_t rbytes = static_cast<size_t>(H) * (bf16 ? 2 : 4);
   bool want_rows = rbytes < 12 * 1024;
-  bool tma_store = rbytes >= 16 * 1024;
-  // The flat engine moves the most bytes per SM when it runs alone under a
-  // budget (66 vs 48-57 GB/s/SM, profiles/k2_engines_r01.txt), but next to
-  // cuBLAS GEMMs (the weave) the TMA engine -- few threads, traffic issued by
-  // the bulk engine -- measured faster (1448 vs 1522 us per Llama layer), so
-  // flat is opt-in (TW_K2_ENGINE=flat).
+  bool tma_store = true;
+  // The flat engine (one 1024-thread CTA per row) is opt-in
+  // (TW_K2_ENGINE=flat): under an SM budget it moves 33 GB/s per SM against
+  // 72 for the two-group TMA engine.
   bool want_flat = false;
   if (engine_env) {
     want_rows = std::strcmp(engine_env, "rows") == 0;
@@ -357,13 +357,10 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
     RowPlan bp;
     const uint32_t row_bytes = static_cast<uint32_t>(H * (bf16 ? 2 : 4));
     static const char* cps_env = std::getenv("TW_K2_CTAS_PER_SM");
-    // Short batches (< ~48 rows per SM) use two CTAs per SM: two consumer
-    // groups per SM cut the pipeline-fill share (T=2048: 24.0 vs 29.1 us,
-    // 4096: 43.2 vs 47.2); long batches keep one CTA with the deeper ring
-    // (8192: 85.1 vs 86.5, 16384: 166.6 vs 172; tools/k2_cps_ab.py).  An
-    // explicit sm_budget keeps one CTA per SM (a ring larger than half the
-    // SM's shared memory cannot co-reside), so the budget really is SMs.
-    int cps = (sm_budget <= 0 && T < 48LL * nsm) ? 2 : 1;
+    // One CTA per SM (an explicit budget really is SMs); concurrency inside
+    // the SM comes from two consumer row groups (below).  TW_K2_CTAS_PER_SM
+    // keeps the older two-CTA half-ring mode for A/B.
+    int cps = 1;
     if (cps_env) cps = std::max(1, std::min(4, std::atoi(cps_env)));
     int stages = static_cast<int>(std::min<size_t>(8, (200 * 1024 / cps) / (2ull * row_bytes)));
     if (stages < 2 && cps > 1) {  // long rows (>= 25 KB): one CTA per SM keeps a 2+ stage ring
@@ -382,9 +379,14 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
       q.H = H;
       q.V = bp.V;
       q.tpr = bp.tpr;
-      // Consumer row groups per CTA (k2_tma_kernel): TW_K2_GROUPS overrides.
+      // Consumer row groups per CTA (k2_tma_kernel), from tools/k2_groups_ab.py:
+      // two groups under an SM budget (72 vs 48 GB/s per SM at H = 8192), for
+      // short batches (< 48 rows per SM: T = 2048 22.6 vs 28.7 us) and for
+      // rows under 16 KB; one group for long batches of >= 16 KB rows (the
+      // deeper per-group ring: T = 16384, H = 8192 161.8 vs 172.0 us).
+      // TW_K2_GROUPS overrides.
       static const char* groups_env = std::getenv("TW_K2_GROUPS");
-      q.groups = 1;
+      q.groups = (sm_budget > 0 || T < 48LL * nsm || row_bytes < 16 * 1024) ? 2 : 1;
       if (groups_env) q.groups = std::max(1, std::min(2, std::atoi(groups_env)));
       if (q.groups * bp.tpr > kBulkMaxConsumers) q.groups = 1;
       q.stages = stages;
