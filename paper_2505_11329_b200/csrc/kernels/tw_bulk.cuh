@@ -78,6 +78,8 @@ struct BulkParams {
   int V;       // 16-byte vectors per row
   int tpr;     // consumer threads per row group (multiple of 32)
   int groups;  // k2_tma_kernel: consumer row groups per CTA (1 or 2; groups * tpr <= 512)
+  int store_lag;  // k2_tma_kernel: 1 = a stage is freed one row late (the store overlaps the next
+                  // row's math), 0 = freed as soon as the bulk engine has read it
   int stages;  // smem ring depth
   uint32_t row_bytes;
   float eps;
@@ -334,17 +336,22 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
       bulk_s2g(static_cast<unsigned char*>(p.out) + row * p.row_bytes, st, p.row_bytes);
       bulk_s2g(static_cast<unsigned char*>(p.res_out) + row * p.row_bytes, st + p.row_bytes, p.row_bytes);
       bulk_commit();
-      // this storer's previous row's stores have finished reading their stage: free it
-      if (prev >= 0) {
-        bulk_wait_read<1>();
-        mbar_arrive(&empty[prev % S]);
+      if (p.store_lag) {
+        // this storer's previous row's stores have finished reading their stage: free it
+        if (prev >= 0) {
+          bulk_wait_read<1>();
+          mbar_arrive(&empty[prev % S]);
+        }
+      } else {
+        bulk_wait_read<0>();  // the bulk engine has read this stage: back to the producer now
+        mbar_arrive(&empty[s]);
       }
     }
     prev = i;
   }
   if (storer) {
     bulk_wait_all();
-    if (prev >= 0) mbar_arrive(&empty[prev % S]);
+    if (p.store_lag && prev >= 0) mbar_arrive(&empty[prev % S]);
   }
 }
 
