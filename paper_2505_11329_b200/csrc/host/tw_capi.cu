@@ -389,8 +389,6 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
       q.groups = (sm_budget > 0 || T < 48LL * nsm || row_bytes < 16 * 1024) ? 2 : 1;
       if (groups_env) q.groups = std::max(1, std::min(2, std::atoi(groups_env)));
       if (q.groups * bp.tpr > kBulkMaxConsumers) q.groups = 1;
-      static const char* lag_env = std::getenv("TW_K2_STORE_LAG");
-      q.store_lag = lag_env ? (std::atoi(lag_env) != 0) : 1;
       q.stages = stages;
       q.row_bytes = row_bytes;
       q.eps = eps;

@@ -78,8 +78,6 @@ struct BulkParams {
   int V;       // 16-byte vectors per row
   int tpr;     // consumer threads per row group (multiple of 32)
   int groups;  // k2_tma_kernel: consumer row groups per CTA (1 or 2; groups * tpr <= 512)
-  int store_lag;  // k2_tma_kernel: 1 = a stage is freed one row late (the store overlaps the next
-                  // row's math), 0 = freed as soon as the bulk engine has read it
   int stages;  // smem ring depth
   uint32_t row_bytes;
   float eps;
@@ -226,9 +224,9 @@ __device__ __forceinline__ void sts_v4(void* p, uint4 v) {
 // after the bulk engine has finished READING it (bulk_wait_read<1> lags one
 // row so the store of row i overlaps the math of row i+1).  The SM's load/
 // store units only touch shared memory; HBM traffic is issued by TMA.
-template <class E, int VPT>
+template <class E, int VPT, int G>
 __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const __grid_constant__ BulkParams p) {
-  // G consumer row groups: group g takes the CTA's rows i = g, g+G, ... (stage
+  // G (template: 1 or 2) consumer row groups: group g takes the CTA's rows i = g, g+G, ... (stage
   // i % S), with its own named barrier, partial-sum slots and storer thread,
   // so G rows are normalised concurrently per SM while the ring keeps up to S
   // rows of loads in flight.  G = 2 roughly doubles what one SM moves when the
@@ -238,7 +236,6 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
   using Acc = typename std::conditional<sizeof(E) == 4, double, float>::type;
   extern __shared__ __align__(128) unsigned char smem[];
   const int S = p.stages;
-  const int G = p.groups;
   unsigned char* ring = smem;  // [S][2][row_bytes]: slot 0 input/output, slot 1 residual/r'
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(S) * 2 * p.row_bytes);
   uint64_t* empty = full + S;
@@ -275,7 +272,7 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     return;
   }
 
-  const int grp = (threadIdx.x - 32) / tpr;
+  const int grp = G == 1 ? 0 : (threadIdx.x - 32) / tpr;
   const int lt = threadIdx.x - 32 - grp * tpr;
   const int cw = lt >> 5;
   const bool storer = lt == 0;
@@ -285,9 +282,7 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     const int c = lt + k * tpr;
     if (c < p.V) load_weight<N>(p.weight, static_cast<long long>(c) * N, w[k]);
   }
-  long long prev = -1;  // this group's previous row index (its stage is released one row late)
-  int parity = 0;
-  for (long long i = grp; i < nrows; i += G, parity ^= 1) {
+  for (long long i = grp; i < nrows; i += G) {
     const int s = static_cast<int>(i % S);
     const uint32_t ph = static_cast<uint32_t>((i / S) & 1);
     const long long row = blockIdx.x + i * gridDim.x;
@@ -313,9 +308,9 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     }
     ss = warp_sum(ss);
     Acc total;
-    Acc* pp = part + (grp * 2 + parity) * cwarps;
+    Acc* pp = part + (grp * 2 + ((i / G) & 1)) * cwarps;
     if (lane == 0) pp[cw] = ss;
-    named_bar_sync(1 + grp, tpr);
+    named_bar_sync(G == 1 ? 1 : 1 + grp, tpr);
     total = 0;
     for (int q = 0; q < cwarps; ++q) total += pp[q];
     const float inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(p.H)) + p.eps);
@@ -331,27 +326,24 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
       }
     }
     fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk engine
-    named_bar_sync(1 + grp, tpr);
+    named_bar_sync(G == 1 ? 1 : 1 + grp, tpr);
     if (storer) {
       bulk_s2g(static_cast<unsigned char*>(p.out) + row * p.row_bytes, st, p.row_bytes);
       bulk_s2g(static_cast<unsigned char*>(p.res_out) + row * p.row_bytes, st + p.row_bytes, p.row_bytes);
       bulk_commit();
-      if (p.store_lag) {
-        // this storer's previous row's stores have finished reading their stage: free it
-        if (prev >= 0) {
-          bulk_wait_read<1>();
-          mbar_arrive(&empty[prev % S]);
-        }
-      } else {
-        bulk_wait_read<0>();  // the bulk engine has read this stage: back to the producer now
-        mbar_arrive(&empty[s]);
+      // this storer's previous row (i - G) has finished reading its stage: free
+      // it (a one-row lag, so the store overlaps the next row's math; freeing
+      // each stage as soon as it is read stalls the group: -10-20 %,
+      // profiles/k2_engines_r01.txt)
+      if (i >= G) {
+        bulk_wait_read<1>();
+        mbar_arrive(&empty[(i - G) % S]);
       }
     }
-    prev = i;
   }
   if (storer) {
     bulk_wait_all();
-    if (p.store_lag && prev >= 0) mbar_arrive(&empty[prev % S]);
+    if (nrows > grp) mbar_arrive(&empty[(grp + (nrows - 1 - grp) / G * G) % S]);
   }
 }
 

@@ -150,15 +150,20 @@ int rownorm_blocks_per_sm(const RowPlan& plan, bool bf16, Xport x) {
 namespace {
 using BulkFn = void (*)(BulkParams);
 
-template <class E>
-BulkFn pick_bulk_e(int vpt, bool tma_store) {
+template <class E, int G>
+BulkFn pick_bulk_eg(int vpt, bool tma_store) {
   switch (vpt) {
-    case 1: return tma_store ? k2_tma_kernel<E, 1> : k2_bulk_kernel<E, 1>;
-    case 2: return tma_store ? k2_tma_kernel<E, 2> : k2_bulk_kernel<E, 2>;
-    case 4: return tma_store ? k2_tma_kernel<E, 4> : k2_bulk_kernel<E, 4>;
-    case 8: return tma_store ? k2_tma_kernel<E, 8> : k2_bulk_kernel<E, 8>;
+    case 1: return tma_store ? k2_tma_kernel<E, 1, G> : k2_bulk_kernel<E, 1>;
+    case 2: return tma_store ? k2_tma_kernel<E, 2, G> : k2_bulk_kernel<E, 2>;
+    case 4: return tma_store ? k2_tma_kernel<E, 4, G> : k2_bulk_kernel<E, 4>;
+    case 8: return tma_store ? k2_tma_kernel<E, 8, G> : k2_bulk_kernel<E, 8>;
     default: return nullptr;
   }
+}
+
+template <class E>
+BulkFn pick_bulk_e(int vpt, bool tma_store, int groups) {
+  return groups == 2 ? pick_bulk_eg<E, 2>(vpt, tma_store) : pick_bulk_eg<E, 1>(vpt, tma_store);
 }
 }  // namespace
 
@@ -169,10 +174,10 @@ size_t bulk_smem_bytes(int stages, uint32_t row_bytes, int tpr, int groups) {
 
 cudaError_t launch_k2_bulk(const BulkParams& params, int vpt, bool bf16, int grid, cudaStream_t stream,
                            bool tma_store) {
-  BulkFn fn = bf16 ? pick_bulk_e<uint16_t>(vpt, tma_store) : pick_bulk_e<float>(vpt, tma_store);
-  if (!fn) return cudaErrorInvalidConfiguration;
   BulkParams p = params;
-  if (!tma_store || p.groups < 1) p.groups = 1;  // the register-store engine has one row group
+  if (!tma_store || p.groups != 2) p.groups = 1;  // the register-store engine has one row group
+  BulkFn fn = bf16 ? pick_bulk_e<uint16_t>(vpt, tma_store, p.groups) : pick_bulk_e<float>(vpt, tma_store, p.groups);
+  if (!fn) return cudaErrorInvalidConfiguration;
   const size_t smem = bulk_smem_bytes(p.stages, p.row_bytes, p.tpr, p.groups);
   cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
