@@ -9,7 +9,6 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
-#include <vector>
 
 #include "tw_internal.h"
 
@@ -111,35 +110,10 @@ tw_status tw_rmsnorm_residual_host(const void* h_input, const void* h_residual, 
   const char* hres = static_cast<const char*>(h_residual);
   char* hro = static_cast<char*>(h_residual_out);
   char* hout = static_cast<char*>(h_output);
-  // Chunk schedule: ramp up (c/16, c/8, c/4, c/2) at the head and back down
-  // at the tail, full chunks between.  The pipeline's exposed time is the
-  // first chunk's H2D and the last chunk's kernel + D2H; small end chunks
-  // shrink both, while the bulk of the rows still moves in the ~8 MiB chunks
-  // that amortise per-copy cost.
-  std::vector<int64_t> sizes;
-  {
-    std::vector<int64_t> ramp;
-    for (int sh = 4; sh >= 1; --sh)
-      if ((chunk_rows >> sh) >= 1) ramp.push_back(chunk_rows >> sh);
-    int64_t ramp_rows = 0;
-    for (int64_t v : ramp) ramp_rows += v;
-    if (!ramp.empty() && T >= 2 * ramp_rows + 2 * chunk_rows) {
-      int64_t mid = T - 2 * ramp_rows;
-      sizes = ramp;
-      while (mid > 0) {
-        const int64_t n = std::min(chunk_rows, mid);
-        sizes.push_back(n);
-        mid -= n;
-      }
-      sizes.insert(sizes.end(), ramp.rbegin(), ramp.rend());
-    } else {
-      for (int64_t r = 0; r < T; r += chunk_rows) sizes.push_back(std::min(chunk_rows, T - r));
-    }
-  }
-  int64_t r0 = 0;
-  for (int64_t k = 0; k < static_cast<int64_t>(sizes.size()); r0 += sizes[static_cast<size_t>(k)], ++k) {
+  int64_t k = 0;
+  for (int64_t r0 = 0; r0 < T; r0 += chunk_rows, ++k) {
     const int slot = static_cast<int>(k % kSlots);
-    const int64_t n = sizes[static_cast<size_t>(k)];
+    const int64_t n = std::min(chunk_rows, T - r0);
     const size_t off = static_cast<size_t>(r0) * row, nb = static_cast<size_t>(n) * row;
     void** b = c.buf[slot];
     // stage 1: H2D, once the slot's previous chunk has drained
