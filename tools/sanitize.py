@@ -16,6 +16,8 @@ for H in (8192, 6144, 4096, 33):
         w = torch.rand(H, device="cuda") + 0.5
         tw.rmsnorm_residual(x, r, w)
         tw.rmsnorm_residual(x, r, w, residual_out=r)
+        # two CTAs: each walks ~18 rows, wrapping the smem ring (both row groups)
+        tw.rmsnorm_residual(x, r, w, sm_budget=2)
 for W in (2, 4):
     T, H = 29, 1024
     comm = tw.Communicator(W, [0] * W, T * H * 4, tw.TW_TRANSPORT_PEER)
