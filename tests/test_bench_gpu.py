@@ -1,0 +1,63 @@
+"""bench.py keeps the driver's contract: one JSON line per run with the keys
+the driver and the judge read, for both arms and under torchrun (two
+processes sharing this box's GPU -- the TP leg's plumbing; its timings are
+meaningless there)."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from tests.conftest import ROOT
+
+BASE_KEYS = {"metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+             "vs_baseline", "dtype", "data", "config"}
+
+
+def _run(args, env=None, timeout=900):
+    p = subprocess.run(args, cwd=ROOT, capture_output=True, text=True, timeout=timeout,
+                       env=dict(os.environ, **(env or {})))
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+def test_bench_single_gpu_line():
+    d = _run([sys.executable, "bench.py", "--steps", "5", "--warmup", "3"])
+    assert BASE_KEYS <= set(d) and d["n_gpus"] == 1 and d["steps"] == 5 and d["warmup"] == 3
+    assert d["higher_is_better"] is False and d["unit"] == "us" and d["value"] > 0
+    assert "workload" in d["config"] and "l2" in d["config"]
+    rf = d["roofline"]
+    assert rf["bound"] == "hbm" and rf["unit"] == "GB/s" and 0 < rf["frac"] <= 1.05
+    assert abs(rf["achieved"] / rf["peak"] - rf["frac"]) < 1e-3
+    e2e = d["e2e"]
+    assert e2e["value"] > d["value"] and e2e["h2d_bytes_per_step"] > 0 and e2e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] == 5
+    assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    cb = d["cpu_baseline"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+
+
+@pytest.mark.gpu
+def test_bench_reference_arm_line():
+    d = _run([sys.executable, "bench.py", "--impl", "reference", "--steps", "2", "--warmup", "3"])
+    assert d["impl"] == "reference" and BASE_KEYS <= set(d)
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    assert d["cpu_baseline"]["value"] == d["value"]
+
+
+@pytest.mark.gpu
+def test_bench_torchrun_two_ranks():
+    """The N>1 leg: torchrun, rank 0 prints the line, max over ranks."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    d = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+              "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3",
+              "--tokens", "1024"], env={"TW_BARRIER_SPIN_LIMIT": str(1 << 28)})
+    assert d["n_gpus"] == 2 and BASE_KEYS <= set(d) and d["value"] > 0
+    assert d["roofline"]["bound"] in ("nvlink", "hbm")
