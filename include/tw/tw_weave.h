@@ -115,6 +115,17 @@ TW_API tw_status tw_weave_throughput(tw_weave_t w, const tw_request* requests, i
                                      unsigned flags, tw_throughput_result* result, double* iteration_latency_s,
                                      int64_t max_iterations);
 
+/* What-if (NOT the product): replace the boundary op by an emulation that
+ * holds `sms` SMs (512-thread CTAs with 160 KB of shared memory, so no GEMM CTA
+ * can share them) for a duration interpolated from a latency table: fused_us
+ * for the fused op (FUSE_ONLY / WEAVE), allreduce_us for the AllReduce of the
+ * unfused baseline (followed by the real add + RMSNorm kernels).  It lets one
+ * GPU measure how the weave schedules a TP = N NVLink-bound op against real
+ * cuBLAS GEMMs, with the op's duration taken from a published multi-GPU table.
+ * n = 0 restores the real op.  tokens strictly increasing. */
+TW_API tw_status tw_weave_emulate_comm(tw_weave_t w, const int64_t* tokens, const float* fused_us,
+                                       const float* allreduce_us, int n, int sms);
+
 /* Per-event timestamps (us from the run's start) of the LAST layer of the
  * last tw_weave_run: op (tw_weave_op), split (0 prefix, 1 suffix, 2 whole),
  * stream (0 compute, 1 boundary).  Arrays hold max_events entries. */

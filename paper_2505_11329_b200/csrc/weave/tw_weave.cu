@@ -86,6 +86,10 @@ struct tw_weave {
   // context output.  Grown on demand outside timed regions.
   int64_t kv_context = 0;
   int64_t kv_cap = 0;
+  // Communication emulation (tw_weave_emulate_comm): published per-token
+  // latency tables of the TP boundary ops; empty = run the real op.
+  std::vector<double> emu_tokens, emu_fused_us, emu_ar_us;
+  int emu_sms = 16;
   void *KV = nullptr, *SC = nullptr, *CO = nullptr;
 };
 
@@ -229,6 +233,41 @@ tw_status ffn(tw_weave* w, int64_t r0, int64_t n) {
   return TW_OK;
 }
 
+// ---- communication emulation (what-if, NOT the product) -----------------------
+// Occupies `sms` SMs for `ns` nanoseconds: 512-thread CTAs holding 160 KB of
+// shared memory each, so no GEMM CTA can share their SM while they spin --
+// the SM footprint of an NVLink-bound fused op whose duration is taken from a
+// published latency table.
+constexpr int kEmuSmem = 160 * 1024;
+__global__ void __launch_bounds__(512, 1) comm_emulation_kernel(unsigned long long ns) {
+  extern __shared__ unsigned char hold[];
+  if (threadIdx.x == 0) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    do {
+      __nanosleep(200);
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    } while (t - t0 < ns);
+    hold[0] = 0;
+  }
+}
+
+// Piecewise-linear interpolation of a latency table at n tokens (linear
+// extrapolation past either end).
+double emu_interp(const std::vector<double>& xs, const std::vector<double>& ys, double n) {
+  if (xs.size() == 1) return ys[0];
+  size_t k = 1;
+  while (k + 1 < xs.size() && xs[k] < n) ++k;
+  const double t = (n - xs[k - 1]) / (xs[k] - xs[k - 1]);
+  return std::max(0.0, ys[k - 1] + t * (ys[k] - ys[k - 1]));
+}
+
+tw_status emulate(tw_weave* w, double us, cudaStream_t s) {
+  comm_emulation_kernel<<<w->emu_sms, 512, kEmuSmem, s>>>(static_cast<unsigned long long>(us * 1e3));
+  CUDA_TRY(cudaGetLastError());
+  return TW_OK;
+}
+
 // Layer-boundary op on rows [r0, r0+n).
 //  * single device: K2 reading the partial sums P, updating the residual R in
 //    place and writing the normed hidden X;
@@ -238,6 +277,7 @@ tw_status ffn(tw_weave* w, int64_t r0, int64_t n) {
 //    lands in every rank's OUTPUT (= X).
 tw_status fused(tw_weave* w, int64_t r0, int64_t n, int budget, cudaStream_t s) {
   if (n <= 0) return TW_OK;
+  if (!w->emu_tokens.empty()) return emulate(w, emu_interp(w->emu_tokens, w->emu_fused_us, double(n)), s);
   const int64_t H = w->spec.hidden;
   char* P = static_cast<char*>(w->P);
   char* R = static_cast<char*>(w->R);
@@ -304,7 +344,10 @@ tw_status unfused(tw_weave* w, int64_t r0, int64_t n, cudaStream_t s) {
   char* P = static_cast<char*>(w->P);
   char* R = static_cast<char*>(w->R);
   char* X = static_cast<char*>(w->X);
-  if (w->comm) {
+  if (!w->emu_tokens.empty()) {
+    // emulated AllReduce, then the real residual add and RMSNorm over all n rows
+    TW_TRY(emulate(w, emu_interp(w->emu_tokens, w->emu_ar_us, double(n)), s));
+  } else if (w->comm) {
     // TP >= 2: the one-shot AllReduce (K3) INPUT -> OUTPUT first; the residual
     // is replicated (every rank adds and normalises all rows), as in an
     // unfused engine.
@@ -326,6 +369,28 @@ tw_status unfused(tw_weave* w, int64_t r0, int64_t n, cudaStream_t s) {
 extern "C" {
 
 const char* tw_weave_last_error(void) { return g_err; }
+
+tw_status tw_weave_emulate_comm(tw_weave_t w, const int64_t* tokens, const float* fused_us, const float* allreduce_us,
+                                int n, int sms) {
+  if (!w) return werr(TW_ERR_CONFIG, "weave_emulate_comm: null runner");
+  w->emu_tokens.clear();
+  w->emu_fused_us.clear();
+  w->emu_ar_us.clear();
+  if (n <= 0) return TW_OK;  // back to the real boundary op
+  if (!tokens || !fused_us || !allreduce_us || sms < 1)
+    return werr(TW_ERR_CONFIG, "weave_emulate_comm: null table or sms < 1");
+  for (int i = 0; i < n; ++i) {
+    if (i > 0 && tokens[i] <= tokens[i - 1])
+      return werr(TW_ERR_CONFIG, "weave_emulate_comm: tokens must increase");
+    w->emu_tokens.push_back(double(tokens[i]));
+    w->emu_fused_us.push_back(fused_us[i]);
+    w->emu_ar_us.push_back(allreduce_us[i]);
+  }
+  w->emu_sms = sms;
+  CUDA_TRY(cudaSetDevice(w->device));
+  CUDA_TRY(cudaFuncSetAttribute(comm_emulation_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kEmuSmem));
+  return TW_OK;
+}
 
 static tw_status weave_create(const tw_layer_spec* spec, int64_t max_tokens, int device, tw_comm_t comm,
                               tw_weave_t* out);

@@ -196,6 +196,9 @@ def _weave_lib():
                                         c_int, c_int, ctypes.c_uint, POINTER(ThroughputResult), POINTER(c_double),
                                         c_int64]
     lib.tw_weave_throughput.restype = c_int
+    lib.tw_weave_emulate_comm.argtypes = [c_void_p, POINTER(c_int64), POINTER(c_float), POINTER(c_float), c_int,
+                                          c_int]
+    lib.tw_weave_emulate_comm.restype = c_int
     lib.tw_weave_last_error.restype = ctypes.c_char_p
     lib.tw_weave_last_error.argtypes = []
     lib.tw_weave_trace.argtypes = [c_void_p, c_int, POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_int),
@@ -272,6 +275,15 @@ class LayerRunner:
                 "total_tokens": res.total_tokens, "total_seconds": res.total_seconds,
                 "mean_iteration_latency": res.mean_iteration_latency,
                 "iteration_latencies": [lat[i] for i in range(min(n_iter, res.iterations))]}
+
+    def emulate_comm(self, tokens=(), fused_us=(), allreduce_us=(), sms: int = 16):
+        """What-if: the boundary op becomes an SM-holding emulation with the
+        table's latency (tw_weave_emulate_comm); no arguments = the real op."""
+        n = len(tokens)
+        t = (c_int64 * max(n, 1))(*tokens)
+        f = (c_float * max(n, 1))(*fused_us)
+        a = (c_float * max(n, 1))(*allreduce_us)
+        self._check(self._L.tw_weave_emulate_comm(self._h, t, f, a, n, sms))
 
     def trace(self, max_events: int = 64):
         n = c_int()

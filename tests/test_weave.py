@@ -137,3 +137,25 @@ def test_k1_token_offset_split_ops(cuda, orc):
         assert_bf16_close(comm.buffer(r, 1, (T, H), torch.bfloat16).float().cpu().numpy(), want_out)
     assert np.array_equal(torch.cat(shards_all).float().cpu().numpy(), bf16_round(np.concatenate(want_res)))
     comm.close()
+
+
+@pytest.mark.gpu
+def test_comm_emulation_what_if(cuda):
+    """tw_weave_emulate_comm: the boundary op holds its SMs for the table's
+    latency (interpolated), fuse-only pays it twice per layer; an empty table
+    restores the real op."""
+    from paper_2505_11329_b200 import weave
+    r = weave.LayerRunner("llama-70b", tp=8, max_tokens=2048)
+    try:
+        nocomm = min(r.run(1024, "nocomm", layers=4) for _ in range(2))
+        real = min(r.run(1024, "fuseonly", layers=4) for _ in range(2))
+        r.emulate_comm([512, 1024, 2048], [200.0, 300.0, 500.0], [150.0, 250.0, 450.0], sms=16)
+        emu = min(r.run(1024, "fuseonly", layers=4) for _ in range(2))
+        assert emu >= nocomm + 2 * 300.0 * 0.95, (nocomm, emu)
+        assert r.run(1024, "tokenweave", prefix=512, boundary_sms=16, layers=2) > 0
+        assert r.run(1024, "unfused", layers=2) >= nocomm + 2 * 250.0 * 0.95
+        r.emulate_comm()
+        back = min(r.run(1024, "fuseonly", layers=4) for _ in range(2))
+        assert back < nocomm + 200.0 and abs(back - real) < 0.25 * real, (real, back)
+    finally:
+        r.close()
