@@ -40,6 +40,9 @@ def main():
     ap.add_argument("--boundary-sms", type=int, default=64)
     ap.add_argument("--graph", action="store_true", help="time each batch's layers as one CUDA-graph replay")
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--emulate-comm", action="store_true",
+                    help="what-if: boundary op = emulation holding --boundary-sms SMs for the paper's 8xB200 "
+                         "fused / AllReduce latency (tw_weave_emulate_comm), one GPU only")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
 
@@ -73,6 +76,8 @@ def main():
            "boundary_op": "K1 (fused AR+residual+RMSNorm)" if world > 1 else "K2 (fused residual+RMSNorm)",
            "iteration": "measured per-layer device time (CUDA events, warm-up layer excluded) x num_layers",
            "layers_measured": args.layers_measured, "boundary_sms": args.boundary_sms, "cuda_graph": args.graph,
+           "emulated_comm": "paper's 8xB200 fused/AllReduce latencies, SMs held (what-if)" if args.emulate_comm
+           else None,
            "rows": []}
     for case in cases:
         model = case["model"]
@@ -88,6 +93,12 @@ def main():
             comm = h
             kw["comm"] = h
         r = weave.LayerRunner(model, tp=tp, max_tokens=max_t, **kw)
+        if args.emulate_comm:
+            with open(os.path.join(ROOT, "profiles", "microbench_b200_measured.json")) as f:
+                ser = json.load(f)["series"]
+            ar = {p["tokens"]: p["microseconds"] for p in ser["allreduce"]}
+            r.emulate_comm([p["tokens"] for p in ser["fused"]], [p["microseconds"] for p in ser["fused"]],
+                           [ar[p["tokens"]] for p in ser["fused"]], args.boundary_sms)
         row = {"name": case["name"], "model": model, "requests": len(reqs),
                "prompt_tokens": sum(p for p, _, _ in reqs), "output_tokens": sum(o for _, o, _ in reqs),
                "chunk_size": case["chunk_size"], "iterations": len(batches),
