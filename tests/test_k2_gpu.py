@@ -24,7 +24,7 @@ def run_k2(inp, res, w, dtype, eps=1e-5, sm_budget=0, inplace=False):
 
 
 @pytest.mark.parametrize("T,H", [(1, 8), (5, 16), (17, 33), (64, 128), (3, 1024), (33, 4096), (64, 8192),
-                                 (7, 12), (9, 24), (2, 16384)])
+                                 (7, 12), (9, 24), (2, 16384), (1000, 4096)])
 def test_k2_fp32_matches_oracle(cuda, orc, T, H):
     inp, res, w = norm_inputs(11 + T * 7 + H, T, H)
     want_out, want_res = orc.rmsnorm_residual(inp, res, w)
@@ -34,8 +34,10 @@ def test_k2_fp32_matches_oracle(cuda, orc, T, H):
     assert_abs_close(out, want_out, 1e-5)
 
 
+# (2048, 6144) and (1500, 8192): many rows per CTA, so the two-row-group TMA
+# engine wraps its smem ring and alternates groups (the default below 48 rows/SM).
 @pytest.mark.parametrize("T,H", [(1, 8), (5, 16), (17, 33), (64, 128), (64, 8192), (7, 24), (256, 8192),
-                                 (4, 6144), (3, 16384)])
+                                 (4, 6144), (3, 16384), (2048, 6144), (1500, 8192)])
 def test_k2_bf16_matches_oracle(cuda, orc, T, H):
     import torch
     inp, res, w = norm_inputs(5 + T + H, T, H)
