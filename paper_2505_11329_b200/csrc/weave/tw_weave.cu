@@ -90,6 +90,7 @@ struct tw_weave {
   // latency tables of the TP boundary ops; empty = run the real op.
   std::vector<double> emu_tokens, emu_fused_us, emu_ar_us;
   int emu_sms = 16;
+  int prio_hi = 0;  // greatest stream priority (the boundary stream's)
   void *KV = nullptr, *SC = nullptr, *CO = nullptr;
 };
 
@@ -268,6 +269,27 @@ tw_status emulate(tw_weave* w, double us, cudaStream_t s) {
   return TW_OK;
 }
 
+// While a CUDA graph is being captured: give the kernel node(s) just captured
+// on the boundary stream that stream's priority.  Stream priority is not
+// carried into captured kernel nodes, so without this a replayed boundary op
+// queues behind the GEMMs' CTAs (the graph is instantiated with
+// cudaGraphInstantiateFlagUseNodePriority).
+void prioritize_captured(tw_weave* w, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t n = 0;
+  if (cudaStreamGetCaptureInfo(s, &st, nullptr, nullptr, &deps, &n) != cudaSuccess ||
+      st != cudaStreamCaptureStatusActive)
+    return;
+  for (size_t i = 0; i < n; ++i) {
+    cudaGraphNodeType t;
+    if (cudaGraphNodeGetType(deps[i], &t) != cudaSuccess || t != cudaGraphNodeTypeKernel) continue;
+    cudaLaunchAttributeValue v = {};
+    v.priority = w->prio_hi;
+    cudaGraphKernelNodeSetAttribute(deps[i], cudaLaunchAttributePriority, &v);
+  }
+}
+
 // Layer-boundary op on rows [r0, r0+n).
 //  * single device: K2 reading the partial sums P, updating the residual R in
 //    place and writing the normed hidden X;
@@ -275,7 +297,15 @@ tw_status emulate(tw_weave* w, double us, cudaStream_t s) {
 //    (token_offset = r0): the split's token_shard_map gives this rank's rows,
 //    whose residual lives at R + (r0 + b_rank) * H; the replicated output
 //    lands in every rank's OUTPUT (= X).
+tw_status fused_op(tw_weave* w, int64_t r0, int64_t n, int budget, cudaStream_t s);
+
 tw_status fused(tw_weave* w, int64_t r0, int64_t n, int budget, cudaStream_t s) {
+  const tw_status st = fused_op(w, r0, n, budget, s);
+  if (st == TW_OK && s == w->boundary) prioritize_captured(w, s);
+  return st;
+}
+
+tw_status fused_op(tw_weave* w, int64_t r0, int64_t n, int budget, cudaStream_t s) {
   if (n <= 0) return TW_OK;
   if (!w->emu_tokens.empty()) return emulate(w, emu_interp(w->emu_tokens, w->emu_fused_us, double(n)), s);
   const int64_t H = w->spec.hidden;
@@ -474,6 +504,7 @@ static tw_status weave_create(const tw_layer_spec* spec, int64_t max_tokens, int
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
   CUDA_TRY(cudaStreamCreateWithPriority(&w->compute, cudaStreamNonBlocking, lo));
   CUDA_TRY(cudaStreamCreateWithPriority(&w->boundary, cudaStreamNonBlocking, hi));
+  w->prio_hi = hi;
   CUBLAS_TRY(cublasCreate(&w->blas));
   CUBLAS_TRY(cublasSetStream(w->blas, w->compute));
   CUDA_TRY(cudaEventCreate(&w->t0));
