@@ -1,14 +1,16 @@
-# For an N-GPU box (not runnable on a one-GPU box): NVLink bytes, DRAM bytes
-# and device time of the fused op K1 on rank 0, per launch, while every rank
-# runs bench.py's TP leg.  Metric names from `ncu --query-metrics --chip gb100`
-# on this pod (profiles/ncu_nvlink_metrics_b200.txt).  ncu serialises and
-# replays the kernel, so only the BYTES are meaningful here, not the time;
-# per-direction NVLink GB/s = nvltx__bytes (egress) / nvlrx__bytes (ingress)
-# over bench.py's own device time.
+# For an N-GPU NVSwitch box (not runnable on a one-GPU box): NVLink bytes moved
+# by bench.py's TP leg, from the driver's per-link throughput counters
+# (`nvidia-smi nvlink -gt d`, TX/RX data payload in KiB) sampled before and
+# after the run -- no kernel replay (ncu replays a kernel once per metric
+# pass, and a replayed K1 waits forever on peers that are not replayed; a
+# two-process trial on one GPU hung that way).  Divide by bench.py's own
+# device time (max over ranks) for NVLink GB/s per GPU per direction, to set
+# against B = S*(G + 1/N) and 900 GB/s.
 N=${1:-8}
+STEPS=${2:-20}
+mkdir -p gpurun_out
+nvidia-smi nvlink -gt d > gpurun_out/nvlink_before.txt
 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29531 \
-  tools/ncu_rank0.py \
-  ncu --target-processes all --clock-control none -k regex:rownorm_kernel -c 3 \
-      --metrics gpu__time_duration.sum,nvltx__bytes.sum,nvlrx__bytes.sum,dram__bytes_read.sum,dram__bytes_write.sum,launch__grid_size \
-      --csv --log-file gpurun_out/k1_nvlink_rank0.csv \
-  -- python bench.py --gpus $N --steps 3 --warmup 3
+  bench.py --gpus $N --steps $STEPS --warmup 3 > gpurun_out/bench_tp$N.json
+nvidia-smi nvlink -gt d > gpurun_out/nvlink_after.txt
+python tools/nvlink_delta.py gpurun_out/nvlink_before.txt gpurun_out/nvlink_after.txt
