@@ -56,3 +56,29 @@ def test_k1_k3_soak_random_launches(cuda):
     comm.check()
     comm.close()
     assert checked == 600
+
+
+def test_k2_soak_random_launches(cuda):
+    """K2 under the shipped engine policy: 400 random (T, H, dtype, SM budget,
+    in-place) launches -- engine, row-group count and ring wrap change from
+    launch to launch -- each against a torch fp32 restatement (residual
+    bitwise to RNE, output to the north_star tolerance)."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    rng = random.Random(4321)
+    for it in range(400):
+        dt = rng.choice([torch.bfloat16, torch.float32])
+        H = rng.choice([8, 33, 1024, 4096, 6144, 8192])
+        T = rng.choice([1, 2, 7, 64, 300, 1024, 2500])
+        budget = rng.choice([0, 0, 1, 2, 8, 33, 148])
+        inplace = rng.random() < 0.3
+        x = torch.randn(T, H, device="cuda").to(dt)
+        r = torch.randn(T, H, device="cuda").to(dt)
+        w = torch.rand(H, device="cuda") + 0.5
+        rp = (x.float() + r.float()).to(dt).float()
+        want = rp * torch.rsqrt((rp * rp).mean(1, keepdim=True) + 1e-5) * w
+        out, rout = tw.rmsnorm_residual(x, r, w, residual_out=r if inplace else None, sm_budget=budget)
+        torch.cuda.synchronize()
+        assert torch.equal(rout.float(), rp), (it, T, H, dt, budget)
+        rel = ((out.float() - want).abs() / torch.maximum(want.abs(), want.pow(2).mean(1, keepdim=True).sqrt())).max()
+        assert rel.item() <= (1e-5 if dt == torch.float32 else 2e-2), (it, T, H, dt, budget, rel.item())
