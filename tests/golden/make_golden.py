@@ -119,8 +119,9 @@ def main() -> None:
         meta["plans"].append({"profile": prof, "model": model, "T": t, "prefix": plan[0], "suffix": plan[1],
                               "offset": plan[2], "mode": plan[3], "num_sms": geom[0], "tile_tokens": geom[1],
                               "cta_columns": geom[2], "threshold": geom[3]})
-    for model in ("llama-70b", "mixtral-8x22b"):
-        for t in (1024, 2048, 4096, 8192):
+    for model, toks in (("llama-70b", (1024, 2048, 4096, 8192)), ("mixtral-8x22b", (1024, 2048, 4096, 8192)),
+                        ("qwen-72b", (256, 512, 1024, 2048, 4096, 8192, 16384))):
+        for t in toks:
             row = {"model": model, "T": t}
             for mode in ("multimem", "fuseonly", "tokenweave", "nocomm"):
                 row[mode] = ref.layer_latency("b200", model, t, mode)

@@ -38,7 +38,9 @@ def main():
     res = {"what": "weave with an EMULATED TP=8 boundary op (published 8xB200 latencies, "
                    f"{args.sms} SMs held) against real cuBLAS GEMMs at TP=8 per-GPU shapes, 1x B200",
            "sms_held": args.sms, "layers_timed": args.layers, "cuda_graph": args.graph, "rows": []}
-    for model, tokens in (("llama-70b", [1024, 2048, 4096, 8192]), ("mixtral-8x22b", [4096, 8192])):
+    # Llama / Mixtral layer shapes, and the Qwen2.5-72B token sweep of BASELINE configs[2]
+    for model, tokens in (("llama-70b", [1024, 2048, 4096, 8192]), ("mixtral-8x22b", [4096, 8192]),
+                          ("qwen-72b", [256, 512, 1024, 2048, 4096, 8192, 16384])):
         r = weave.LayerRunner(model, tp=8, max_tokens=max(tokens))
         r.emulate_comm(toks, fused, ar, args.sms)
         for T in tokens:
