@@ -333,6 +333,18 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
   // (TW_K2_ENGINE=flat): under an SM budget it moves 33 GB/s per SM against
   // 72 for the two-group TMA engine.
   bool want_flat = false;
+  // Decode-size batches of long rows (tools/k2_small_graph.py, H = 8192 bf16,
+  // CUDA-graph replay / cold): up to one row per SM the flat engine (one row
+  // per CTA, no ring to set up) is fastest -- 2.9-3.3 vs 3.7-4.1 us replayed,
+  // 8.2 vs 8.2-10.2 us cold; up to two rows per SM the register row engine
+  // (4.1 vs 5.1 us replayed at T = 256).  Whole-GPU launches only.
+  if (!engine_env && sm_budget <= 0 && !want_rows && vec) {
+    if (T <= nsm && H / nv <= 2048) {
+      want_flat = true;
+    } else if (T <= 2LL * nsm) {
+      want_rows = true;
+    }
+  }
   if (engine_env) {
     want_rows = std::strcmp(engine_env, "rows") == 0;
     tma_store = std::strcmp(engine_env, "tma") == 0;
