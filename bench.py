@@ -352,6 +352,21 @@ def run_ours_single(args):
         # simulated ranks share this GPU: the whole GPU (2 CTAs/SM) split between them
         line["k1_colocated_peer_us"] = {f"tp{n}_ctas{296 // n}": k1_colocated(T, H, n, 296 // n, flush)
                                         for n in (2, 8)}
+        # the weave: one Llama-3.3-70B layer at TP = 8 per-GPU
+        # GEMM shapes, T = 8192, boundary op K2 (the one-GPU stand-in for K1)
+        try:
+            from paper_2505_11329_b200 import weave
+            r = weave.LayerRunner("llama-70b", tp=8, max_tokens=T)
+            a, _, _, _ = weave.make_split_plan(T, threshold=r.threshold)
+            line["weave_llama70b_tp8_shapes_us"] = {
+                "T": T, "unfused": round(r.run(T, "unfused", layers=6), 1),
+                "fuseonly": round(r.run(T, "fuseonly", layers=6), 1),
+                "tokenweave": round(min(r.run(T, "tokenweave", prefix=a, boundary_sms=b, layers=6) for b in (32, 64)), 1),
+                "nocomm": round(r.run(T, "nocomm", layers=6), 1),
+                "note": "per-layer device time, eager launches; GEMMs are cuBLAS load (not product)"}
+            r.close()
+        except Exception as exc:  # libtw_weave / cuBLAS unavailable: report, do not fail the bench
+            line["weave_llama70b_tp8_shapes_us"] = {"error": str(exc)[:200]}
         threads = os.cpu_count() or 1
         sample_T = 2048
         cpu_ms = reference_rmsnorm_ms(sample_T, H, threads, 3)
