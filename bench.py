@@ -361,7 +361,8 @@ def run_ours_single(args):
             line["weave_llama70b_tp8_shapes_us"] = {
                 "T": T, "unfused": round(r.run(T, "unfused", layers=6), 1),
                 "fuseonly": round(r.run(T, "fuseonly", layers=6), 1),
-                "tokenweave": round(min(r.run(T, "tokenweave", prefix=a, boundary_sms=b, layers=6) for b in (32, 64)), 1),
+                "tokenweave": round(min(r.run(T, "tokenweave", prefix=a, boundary_sms=b, layers=6)
+                                        for b in (16, 32, 64)), 1),
                 "nocomm": round(r.run(T, "nocomm", layers=6), 1),
                 "note": "per-layer device time, eager launches; GEMMs are cuBLAS load (not product)"}
             r.close()
