@@ -205,8 +205,12 @@ def k2_timed(T, H, steps, warmup, flush, seed=0):
     w = torch.rand(H, device=dev, generator=g) + 0.5
     out, rout = torch.empty_like(x), torch.empty_like(x)
     stream = torch.cuda.Stream()
+    # warm-up = the timed loop's exact sequence (flush, then the op), so the
+    # first timed step does not pay the flush path's first-use costs (it ran
+    # ~140 us instead of ~85 when the warm-up skipped the flush)
     with torch.cuda.stream(stream):
-        for _ in range(max(warmup, 3)):
+        for i in range(max(warmup, 3)):
+            flush(i)
             tw.rmsnorm_residual(x, r, w, EPS, residual_out=rout, out=out, stream=stream)
     torch.cuda.synchronize()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
