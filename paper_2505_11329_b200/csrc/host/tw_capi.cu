@@ -298,6 +298,44 @@ tw_status tw_shard_map_validate(const int64_t* ranges, int world, int64_t total_
   return TW_OK;
 }
 
+namespace {
+
+// K2 engines (profiles/k2_engines_r01.txt has every A/B behind this policy):
+//   Flat  one row per 1024-thread CTA, registers only
+//   Rows  the register row engine of tw_rownorm.cuh (also K1's engine)
+//   Tma   bulk-copy ring, bulk loads + bulk stores (k2_tma_kernel)
+//   Bulk  bulk loads + register stores (k2_bulk_kernel; A/B only)
+enum class K2Engine { Flat, Rows, Tma, Bulk };
+
+K2Engine choose_k2_engine(int64_t T, int64_t H, bool bf16, bool vec, int nsm, int sm_budget) {
+  static const char* engine_env = std::getenv("TW_K2_ENGINE");
+  if (engine_env) {
+    if (std::strcmp(engine_env, "rows") == 0) return K2Engine::Rows;
+    if (std::strcmp(engine_env, "tma") == 0) return K2Engine::Tma;
+    if (std::strcmp(engine_env, "flat") == 0) return K2Engine::Flat;
+    return K2Engine::Bulk;
+  }
+  const int nv = bf16 ? 8 : 4;
+  const size_t rbytes = static_cast<size_t>(H) * (bf16 ? 2 : 4);
+  // Rows under 12 KB: the register row engine (per-row barrier and bulk-issue
+  // costs dominate short rows).  Rows >= 12 KB: the TMA engine (with two
+  // consumer row groups it beats the register-store variant at 12 KB rows:
+  // H = 6144 bf16, T = 4096: 30.8 vs 41.0 us, tools/k2_groups_ab.py).
+  if (!vec || rbytes < 12 * 1024) return K2Engine::Rows;
+  // Decode-size batches on the whole GPU (tools/k2_small_graph.py, H = 8192
+  // bf16): up to one row per SM the flat engine (no ring to set up; 2.9-3.3 vs
+  // 3.7-4.1 us replayed in a CUDA graph, 8.2 vs 8.2-10.2 us cold), up to two
+  // rows per SM the row engine (4.1 vs 5.1 us replayed at T = 256).  Under an
+  // SM budget the TMA engine moves the most per SM (72 GB/s vs 33 for flat).
+  if (sm_budget <= 0) {
+    if (T <= nsm && H / nv <= 2048) return K2Engine::Flat;
+    if (T <= 2LL * nsm) return K2Engine::Rows;
+  }
+  return K2Engine::Tma;
+}
+
+}  // namespace
+
 tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* residual_out, void* output,
                               const float* weight, int64_t T, int64_t H, float eps, tw_dtype dtype, int sm_budget,
                               void* stream) {
@@ -317,39 +355,10 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
   cudaGetDevice(&dev);
   const int nsm = sm_count(dev);
   const int sms = sm_budget > 0 ? std::min(sm_budget, nsm) : nsm;
-  // Preferred engine: the warp-specialised bulk-copy pipeline (16-B aligned
-  // rows, H % (16/elem) == 0).  TW_K2_ENGINE=rows forces the row engine.
-  static const char* engine_env = std::getenv("TW_K2_ENGINE");
-  // Default by row size (measured on B200, profiles/k2_engines_r01.txt): rows
-  // >= 12 KB -> the TMA engine (bulk loads + bulk stores); smaller rows -> the
-  // register row engine (per-row barrier and bulk issue costs dominate short
-  // rows).  The TMA engine with two consumer row groups beats the
-  // register-store variant at 12 KB rows (H = 6144 bf16: 30.8 vs 41.0 us at
-  // T = 4096, tools/k2_groups_ab.py), which is kept for A/B (TW_K2_ENGINE=bulk).
-  const size_t rbytes = static_cast<size_t>(H) * (bf16 ? 2 : 4);
-  bool want_rows = rbytes < 12 * 1024;
-  bool tma_store = true;
-  // The flat engine (one 1024-thread CTA per row) is opt-in
-  // (TW_K2_ENGINE=flat): under an SM budget it moves 33 GB/s per SM against
-  // 72 for the two-group TMA engine.
-  bool want_flat = false;
-  // Decode-size batches of long rows (tools/k2_small_graph.py, H = 8192 bf16,
-  // CUDA-graph replay / cold): up to one row per SM the flat engine (one row
-  // per CTA, no ring to set up) is fastest -- 2.9-3.3 vs 3.7-4.1 us replayed,
-  // 8.2 vs 8.2-10.2 us cold; up to two rows per SM the register row engine
-  // (4.1 vs 5.1 us replayed at T = 256).  Whole-GPU launches only.
-  if (!engine_env && sm_budget <= 0 && !want_rows && vec) {
-    if (T <= nsm && H / nv <= 2048) {
-      want_flat = true;
-    } else if (T <= 2LL * nsm) {
-      want_rows = true;
-    }
-  }
-  if (engine_env) {
-    want_rows = std::strcmp(engine_env, "rows") == 0;
-    tma_store = std::strcmp(engine_env, "tma") == 0;
-    want_flat = std::strcmp(engine_env, "flat") == 0;
-  }
+  const K2Engine engine = choose_k2_engine(T, H, bf16, vec, nsm, sm_budget);
+  const bool want_flat = engine == K2Engine::Flat;
+  const bool want_rows = engine == K2Engine::Rows;
+  const bool tma_store = engine == K2Engine::Tma;
   if (vec && want_flat && H / nv <= 2048) {
     FlatParams f = {};
     f.in = input;
