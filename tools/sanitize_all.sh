@@ -1,3 +1,5 @@
+# compute-sanitizer memcheck / racecheck / synccheck over tools/sanitize.py,
+# TMA engine with one and two row groups and the default policy.
 set -x
 out=gpurun_out/san
 mkdir -p $out
