@@ -3,8 +3,8 @@
  * INFRASTRUCTURE ONLY (see tw_oracle.h): the checker, never the product.
  *
  * Parity pinned against oracle/_ref/libweavesim_ref.so (the reference's own
- * proj/src/{numerics,collectives,wavemodel,splitter}.cpp compiled unmodified,
- * see oracle/Makefile) and against tests/golden/*.npz generated from it by
+ * proj/src/{numerics,collectives,wavemodel,splitter,workloads}.cpp compiled unmodified,
+ * see oracle/Makefile) and against tests/golden/ fixtures generated from it by
  * tests/golden/make_golden.py.  Compile with -ffp-contract=off so the float
  * expression order matches the reference build (no FMA contraction).
  */
