@@ -37,6 +37,23 @@ struct HardwareProfile {
   void validate() const;
 };
 
+// Transformer layer shape; per-GPU work is derived via tp_degree
+// (proj/include/weavesim/wavemodel.hpp:48-60).
+struct LayerSpec {
+  std::int64_t hidden = 8192;
+  std::int64_t intermediate = 28672;
+  int num_attention_heads = 64;
+  int num_kv_heads = 8;
+  int head_dim = 128;
+  int num_layers = 80;
+  int experts = 1;  // 1 = dense
+  int top_k = 1;    // active experts per token
+  int tp_degree = 8;
+
+  // ConfigError on an impossible shape (proj/src/wavemodel.cpp:23-36).
+  void validate() const;
+};
+
 // B200 geometry (148 SMs, the reference's default tile geometry).  Replaces the
 // geometry part of builtin_profile("b200") (proj/src/presets.cpp:58-64).
 HardwareProfile b200_geometry();

@@ -20,6 +20,9 @@
 #include "weavesim/numerics.hpp"
 #include "weavesim/splitter.hpp"
 #include "weavesim/workloads.hpp"
+#include "weavesim/presets.hpp"
+#include "weavesim/scheduler.hpp"
+#include <numeric>
 
 using namespace weavesim;
 
@@ -360,6 +363,48 @@ void workload_cases() {
   CHECK_THROWS_AS(form_batches({}, 0), ConfigError);
   CHECK_THROWS_AS(synth_trace(0, 100, 10), ConfigError);
   CHECK_THROWS_AS(synth_trace(4, 0, 10), ConfigError);
+  // presets / modes / LayerSpec (proj/src/presets.cpp:68-110, scheduler.cpp:16-46, wavemodel.cpp:23-36)
+  CHECK(model_preset("llama-70b").spec.num_layers == 80 && model_preset("mixtral-8x22b").spec.experts == 8);
+  CHECK(model_preset("mixtral-8x22b").policy.threshold_tokens == 4096 && model_preset_names().size() == 3);
+  CHECK_THROWS_AS(model_preset("gpt-5"), ConfigError);
+  CHECK(builtin_profile("b200").num_sms == 148 && builtin_profile("h100").num_sms == 132);
+  CHECK_THROWS_AS(builtin_profile("a100"), ConfigError);
+  for (BaselineMode m : {BaselineMode::Default, BaselineMode::Multimem, BaselineMode::NoComm, BaselineMode::FuseOnly,
+                         BaselineMode::TokenWeave})
+    CHECK(baseline_mode_from_string(to_string(m)) == m);
+  CHECK_THROWS_AS(baseline_mode_from_string("magic"), ConfigError);
+  {
+    LayerSpec bad = model_preset("llama-70b").spec;
+    bad.tp_degree = 1;
+    CHECK_THROWS_AS(bad.validate(), ConfigError);
+    bad = model_preset("llama-70b").spec;
+    bad.num_kv_heads = 7;
+    CHECK_THROWS_AS(bad.validate(), ConfigError);
+  }
+  // simulate_throughput validates before touching a device
+  const ModelPreset pr = model_preset("llama-70b");
+  CHECK_THROWS_AS(simulate_throughput(synth_trace(2, 10, 1), pr.spec, builtin_profile("b200"),
+                                      BaselineMode::TokenWeave, pr.policy, 0),
+                  ConfigError);
+}
+
+// proj/tests/test_workloads.cpp:127-147 on the measured (B200) simulate_throughput.
+void throughput_gpu_cases() {
+  const ModelPreset preset = model_preset("llama-70b");
+  const HardwareProfile profile = builtin_profile("b200");
+  const std::vector<Request> requests = synth_trace(4, 512, 3);
+  const ThroughputResult r =
+      simulate_throughput(requests, preset.spec, profile, BaselineMode::TokenWeave, preset.policy, 1024);
+  CHECK(r.total_tokens == 4 * (512 + 3));
+  CHECK(r.iterations == static_cast<std::int64_t>(r.iteration_latencies.size()));
+  const double sum = std::accumulate(r.iteration_latencies.begin(), r.iteration_latencies.end(), 0.0);
+  CHECK(std::abs(r.total_seconds - sum) <= 1e-12 * sum + 1e-15);
+  CHECK(std::abs(r.tokens_per_sec - r.total_tokens / r.total_seconds) <= 1e-9 * r.tokens_per_sec);
+  const double nocomm =
+      simulate_throughput(requests, preset.spec, profile, BaselineMode::NoComm, preset.policy, 1024).tokens_per_sec;
+  const double multimem =
+      simulate_throughput(requests, preset.spec, profile, BaselineMode::Multimem, preset.policy, 1024).tokens_per_sec;
+  CHECK(nocomm >= multimem);
 }
 
 }  // namespace
@@ -371,6 +416,7 @@ int main(int argc, char** argv) {
   workload_cases();
   if (mode == "gpu") {
     gpu_cases();
+    throughput_gpu_cases();
     acceptance_cases(false);
   }
   if (mode == "acceptance") acceptance_cases(true);
