@@ -3,6 +3,7 @@
 //   LayerSpec::validate            proj/src/wavemodel.cpp:23-36
 //   to_string / baseline_mode_from_string   proj/src/scheduler.cpp:16-46
 //   model_preset / builtin_profile proj/src/presets.cpp:53-110 (geometry only)
+//   iteration_latency              proj/src/scheduler.cpp:387-392, the layer RUN
 //   simulate_throughput            proj/src/workloads.cpp:111-141, every batch
 //                                  RUN through the layer runner
 // The runner lives in libtw_weave.so, which links this library; it is loaded
@@ -125,7 +126,82 @@ const WeaveApi& weave_api() {
   throw DeviceError(msg);
 }
 
+// One runner per process, reused while the layer shape matches and it is
+// large enough (creating one allocates the layer's weights and activations).
+struct RunnerCache {
+  tw_weave_t w = nullptr;
+  tw_layer_spec spec{};
+  std::int64_t max_tokens = 0;
+};
+
+tw_weave_t runner_for(const WeaveApi& api, const LayerSpec& spec, std::int64_t tokens) {
+  static RunnerCache cache;  // intentionally not destroyed at exit (CUDA may be torn down first)
+  const tw_layer_spec ls{spec.hidden, spec.intermediate, spec.num_attention_heads, spec.num_kv_heads, spec.head_dim,
+                         spec.experts, spec.top_k, spec.tp_degree};
+  const bool same = cache.w && cache.spec.hidden == ls.hidden && cache.spec.intermediate == ls.intermediate &&
+                    cache.spec.heads == ls.heads && cache.spec.kv_heads == ls.kv_heads &&
+                    cache.spec.head_dim == ls.head_dim && cache.spec.experts == ls.experts &&
+                    cache.spec.top_k == ls.top_k && cache.spec.tp == ls.tp;
+  if (same && cache.max_tokens >= tokens) return cache.w;
+  if (cache.w) api.destroy(cache.w);
+  cache.w = nullptr;
+  const std::int64_t cap = std::max<std::int64_t>(tokens, same ? 2 * cache.max_tokens : tokens);
+  tw_weave_t w = nullptr;
+  const tw_status st = api.create(&ls, cap, 0, &w);
+  if (st != TW_OK) runner_error(api, st, "weavesim: layer runner");
+  cache.w = w;
+  cache.spec = ls;
+  cache.max_tokens = cap;
+  return w;
+}
+
+const WeaveApi& require_api() {
+  const WeaveApi& api = weave_api();
+  if (!api.create || !api.destroy || !api.run_batch)
+    throw DeviceError("weavesim: libtw_weave.so not found next to libweavesim_b200.so");
+  return api;
+}
+
+// One measured iteration: the mode mapping and TokenWeave degrade rules
+// (decode-only and non-Overlap batches run fuse-only, scheduler.cpp:333-341).
+double measured_iteration(const WeaveApi& api, tw_weave_t w, const BatchShape& batch, const LayerSpec& spec,
+                          const HardwareProfile& profile, BaselineMode mode, const SplitPolicy& policy) {
+  tw_weave_mode m = TW_MODE_UNFUSED;
+  std::int64_t prefix = 0;
+  switch (mode) {
+    case BaselineMode::Default:
+    case BaselineMode::Multimem: m = TW_MODE_UNFUSED; break;
+    case BaselineMode::NoComm: m = TW_MODE_NO_COMM; break;
+    case BaselineMode::FuseOnly: m = TW_MODE_FUSE_ONLY; break;
+    case BaselineMode::TokenWeave: {
+      m = TW_MODE_FUSE_ONLY;
+      if (!batch.decode_only) {
+        const SplitPlan plan = make_split_plan(batch.total_tokens, profile, policy);
+        if (plan.mode == SplitMode::Overlap && plan.suffix_tokens > 0) {
+          m = TW_MODE_WEAVE;
+          prefix = plan.prefix_tokens;
+        }
+      }
+      break;
+    }
+  }
+  float us = 0.0f;
+  const tw_status st = api.run_batch(w, batch.total_tokens, prefix, batch.kv_context, m, 64, 0, 2, 0u, &us);
+  if (st != TW_OK) runner_error(api, st, "weavesim: measured iteration");
+  return 1e-6 * static_cast<double>(us) * spec.num_layers;
+}
+
 }  // namespace
+
+double iteration_latency(const BatchShape& batch, const LayerSpec& spec, const HardwareProfile& profile,
+                         BaselineMode mode, const SplitPolicy& policy) {
+  spec.validate();
+  profile.validate();
+  if (batch.total_tokens < 0 || batch.kv_context < 0) throw DimensionError("iteration_latency: negative batch shape");
+  if (batch.total_tokens == 0) return 0.0;
+  const WeaveApi& api = require_api();
+  return measured_iteration(api, runner_for(api, spec, batch.total_tokens), batch, spec, profile, mode, policy);
+}
 
 ThroughputResult simulate_throughput(const std::vector<Request>& requests, const LayerSpec& spec,
                                      const HardwareProfile& profile, BaselineMode mode, const SplitPolicy& policy,
@@ -135,51 +211,20 @@ ThroughputResult simulate_throughput(const std::vector<Request>& requests, const
   const std::vector<IterationBatch> batches = form_batches(requests, chunk_size);
   ThroughputResult result;
   if (batches.empty()) return result;
-  const WeaveApi& api = weave_api();
-  if (!api.create || !api.destroy || !api.run_batch)
-    throw DeviceError("simulate_throughput: libtw_weave.so not found next to libweavesim_b200.so");
+  const WeaveApi& api = require_api();
   std::int64_t max_t = 0;
   for (const IterationBatch& b : batches) max_t = std::max(max_t, b.total_tokens);
-  tw_layer_spec ls{spec.hidden, spec.intermediate, spec.num_attention_heads, spec.num_kv_heads, spec.head_dim,
-                   spec.experts, spec.top_k, spec.tp_degree};
-  tw_weave_t w = nullptr;
-  tw_status st = api.create(&ls, max_t, 0, &w);
-  if (st != TW_OK) runner_error(api, st, "simulate_throughput: runner");
-  try {
-    for (const IterationBatch& b : batches) {
-      tw_weave_mode m = TW_MODE_UNFUSED;
-      std::int64_t prefix = 0;
-      switch (mode) {
-        case BaselineMode::Default:
-        case BaselineMode::Multimem: m = TW_MODE_UNFUSED; break;
-        case BaselineMode::NoComm: m = TW_MODE_NO_COMM; break;
-        case BaselineMode::FuseOnly: m = TW_MODE_FUSE_ONLY; break;
-        case BaselineMode::TokenWeave: {
-          // decode-only and non-Overlap batches run fuse-only (scheduler.cpp:333-341)
-          m = TW_MODE_FUSE_ONLY;
-          if (!b.decode_only()) {
-            const SplitPlan plan = make_split_plan(b.total_tokens, profile, policy);
-            if (plan.mode == SplitMode::Overlap && plan.suffix_tokens > 0) {
-              m = TW_MODE_WEAVE;
-              prefix = plan.prefix_tokens;
-            }
-          }
-          break;
-        }
-      }
-      float us = 0.0f;
-      st = api.run_batch(w, b.total_tokens, prefix, b.kv_context, m, 64, 0, 2, 0u, &us);
-      if (st != TW_OK) runner_error(api, st, "simulate_throughput: batch");
-      const double latency = 1e-6 * static_cast<double>(us) * spec.num_layers;
-      result.iteration_latencies.push_back(latency);
-      result.total_seconds += latency;
-      result.total_tokens += b.total_tokens;
-    }
-  } catch (...) {
-    api.destroy(w);
-    throw;
+  tw_weave_t w = runner_for(api, spec, max_t);
+  for (const IterationBatch& b : batches) {
+    BatchShape shape;
+    shape.total_tokens = b.total_tokens;
+    shape.kv_context = b.kv_context;
+    shape.decode_only = b.decode_only();
+    const double latency = measured_iteration(api, w, shape, spec, profile, mode, policy);
+    result.iteration_latencies.push_back(latency);
+    result.total_seconds += latency;
+    result.total_tokens += b.total_tokens;
   }
-  api.destroy(w);
   result.iterations = static_cast<std::int64_t>(batches.size());
   if (result.total_seconds > 0.0) result.tokens_per_sec = result.total_tokens / result.total_seconds;
   result.mean_iteration_latency = result.total_seconds / static_cast<double>(result.iterations);

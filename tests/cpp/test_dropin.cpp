@@ -386,6 +386,14 @@ void workload_cases() {
   CHECK_THROWS_AS(simulate_throughput(synth_trace(2, 10, 1), pr.spec, builtin_profile("b200"),
                                       BaselineMode::TokenWeave, pr.policy, 0),
                   ConfigError);
+  {
+    BatchShape neg;
+    neg.total_tokens = -1;
+    CHECK_THROWS_AS(iteration_latency(neg, pr.spec, builtin_profile("b200"), BaselineMode::FuseOnly, pr.policy),
+                    DimensionError);
+    BatchShape empty;
+    CHECK(iteration_latency(empty, pr.spec, builtin_profile("b200"), BaselineMode::FuseOnly, pr.policy) == 0.0);
+  }
 }
 
 // proj/tests/test_workloads.cpp:127-147 on the measured (B200) simulate_throughput.
@@ -405,6 +413,16 @@ void throughput_gpu_cases() {
   const double multimem =
       simulate_throughput(requests, preset.spec, profile, BaselineMode::Multimem, preset.policy, 1024).tokens_per_sec;
   CHECK(nocomm >= multimem);
+  // iteration_latency: measured layer x num_layers; communication costs time
+  BatchShape b;
+  b.total_tokens = 2048;
+  const double nc = iteration_latency(b, preset.spec, profile, BaselineMode::NoComm, preset.policy);
+  const double fo = iteration_latency(b, preset.spec, profile, BaselineMode::FuseOnly, preset.policy);
+  const double mm = iteration_latency(b, preset.spec, profile, BaselineMode::Multimem, preset.policy);
+  const double tw = iteration_latency(b, preset.spec, profile, BaselineMode::TokenWeave, preset.policy);
+  CHECK(nc > 0 && nc < fo && fo < mm && tw > nc);
+  std::printf("iteration_latency (llama-70b, T=2048, 80 layers): nocomm %.2f ms, fuseonly %.2f, multimem %.2f, "
+              "tokenweave %.2f\n", 1e3 * nc, 1e3 * fo, 1e3 * mm, 1e3 * tw);
 }
 
 }  // namespace
