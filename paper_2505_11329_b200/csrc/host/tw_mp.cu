@@ -17,7 +17,10 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
+#include <poll.h>
+#include <sys/time.h>
 #include <string>
 #include <thread>
 #include <vector>
@@ -54,8 +57,18 @@ class Rendezvous {
         *err = std::string("rendezvous: bind/listen failed: ") + std::strerror(errno);
         return false;
       }
+      const auto accept_deadline = std::chrono::steady_clock::now() + std::chrono::seconds(timeout_s());
       for (int n = 1; n < world_; ++n) {
+        // bounded: a rank that failed before reaching the rendezvous must not hang rank 0
+        pollfd pf{listen_fd_, POLLIN, 0};
+        const auto left = std::chrono::duration_cast<std::chrono::milliseconds>(
+            accept_deadline - std::chrono::steady_clock::now()).count();
+        if (left <= 0 || poll(&pf, 1, static_cast<int>(left)) <= 0) {
+          *err = "rendezvous: timed out waiting for peers to connect";
+          return false;
+        }
         const int fd = accept(listen_fd_, nullptr, nullptr);
+        if (fd >= 0) set_timeouts(fd);
         int32_t peer = -1;
         if (fd < 0 || !read_all(fd, &peer, sizeof(peer)) || peer <= 0 || peer >= world_ || peers_[peer] >= 0) {
           *err = "rendezvous: bad peer handshake";
@@ -66,10 +79,11 @@ class Rendezvous {
       }
       return true;
     }
-    const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(120);
+    const auto deadline = std::chrono::steady_clock::now() + std::chrono::seconds(timeout_s());
     while (true) {
       const int fd = socket(AF_UNIX, SOCK_STREAM, 0);
       if (fd >= 0 && connect(fd, reinterpret_cast<sockaddr*>(&addr_), len_) == 0) {
+        set_timeouts(fd);
         const int32_t me = rank_;
         if (!write_all(fd, &me, sizeof(me))) {
           close(fd);
@@ -142,6 +156,22 @@ class Rendezvous {
   }
 
  private:
+  // Bound of every rendezvous wait, seconds (TW_RENDEZVOUS_TIMEOUT_S overrides).
+  static int timeout_s() {
+    static const int t = [] {
+      const char* e = std::getenv("TW_RENDEZVOUS_TIMEOUT_S");
+      const int v = e ? std::atoi(e) : 120;
+      return v > 0 ? v : 120;
+    }();
+    return t;
+  }
+  // Every blocking read/write on a rendezvous socket gives up after the same
+  // bound, so a peer stuck outside the rendezvous surfaces as an error.
+  static void set_timeouts(int fd) {
+    timeval tv{timeout_s(), 0};
+    setsockopt(fd, SOL_SOCKET, SO_RCVTIMEO, &tv, sizeof(tv));
+    setsockopt(fd, SOL_SOCKET, SO_SNDTIMEO, &tv, sizeof(tv));
+  }
   static bool fail_msg(std::string* err, const char* m) {
     *err = m;
     return false;

@@ -74,3 +74,27 @@ def test_nvlink_roofline_bytes():
     assert abs(algorithmic_nvlink_bytes(1024, 8192, 8, False) / 1e6 - 18.87) < 0.01
     assert abs(algorithmic_nvlink_bytes(8192, 8192, 8, False) / 1e6 - 150.99) < 0.01
     assert abs(algorithmic_nvlink_bytes(8192, 8192, 8, True) / 1e6 - 285.21) < 0.01
+
+
+def test_rendezvous_times_out_when_a_peer_never_arrives():
+    """A rank that fails before the rendezvous must not hang the others: rank 0
+    alone (and a rank without rank 0) give up after the bound."""
+    import time
+    code = textwrap.dedent("""
+        import ctypes, sys, time
+        sys.path.insert(0, {root!r})
+        from paper_2505_11329_b200 import _lib
+        out = ctypes.c_int(-1)
+        t0 = time.time()
+        st = _lib.lib.tw_rendezvous_exchange_fd(b"lonely-{tag}", 2, {rank}, -1, ctypes.byref(out))
+        print(st, round(time.time() - t0, 1), _lib.lib.tw_last_error().decode())
+    """)
+    for rank in (0, 1):
+        t0 = time.time()
+        p = subprocess.run([sys.executable, "-c", code.format(root=ROOT, tag=f"{os.getpid()}-{rank}", rank=rank)],
+                           env=dict(os.environ, TW_RENDEZVOUS_TIMEOUT_S="2"), capture_output=True, text=True,
+                           timeout=60)
+        assert p.returncode == 0, p.stderr
+        st, secs, msg = p.stdout.split(" ", 2)
+        assert int(st) == 3 and "timed out" in msg, p.stdout  # TW_ERR_CONFIG
+        assert time.time() - t0 < 30
