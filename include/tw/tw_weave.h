@@ -108,7 +108,10 @@ typedef struct tw_throughput_result {
  * num_layers.  In WEAVE mode decode-only batches and batches make_split_plan
  * (b200 geometry, threshold_tokens) does not split run FUSE_ONLY
  * (scheduler.cpp:333-341).  iteration_latency_s (optional) receives up to
- * max_iterations per-batch latencies in seconds. */
+ * max_iterations per-batch latencies in seconds.  boundary_sm_budget =
+ * TW_WEAVE_AUTO_BUDGET: for each weaved batch size the fused op's SM budget is
+ * measured once over {16, 32, 64} and the fastest reused. */
+#define TW_WEAVE_AUTO_BUDGET (-1)
 TW_API tw_status tw_weave_throughput(tw_weave_t w, const tw_request* requests, int64_t n, int64_t chunk_size,
                                      tw_weave_mode mode, int64_t threshold_tokens, int num_layers,
                                      int layers_measured, int boundary_sm_budget, int gemm_sm_target,

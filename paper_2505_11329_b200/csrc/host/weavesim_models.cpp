@@ -186,8 +186,20 @@ double measured_iteration(const WeaveApi& api, tw_weave_t w, const BatchShape& b
     }
   }
   float us = 0.0f;
-  const tw_status st = api.run_batch(w, batch.total_tokens, prefix, batch.kv_context, m, 64, 0, 2, 0u, &us);
-  if (st != TW_OK) runner_error(api, st, "weavesim: measured iteration");
+  if (m == TW_MODE_WEAVE) {
+    // the fused op's SM budget that schedules best on this box, over 16/32/64
+    float best = 0.0f;
+    for (int cand : {16, 32, 64}) {
+      float t = 0.0f;
+      const tw_status st = api.run_batch(w, batch.total_tokens, prefix, batch.kv_context, m, cand, 0, 2, 0u, &t);
+      if (st != TW_OK) runner_error(api, st, "weavesim: measured iteration");
+      if (best == 0.0f || t < best) best = t;
+    }
+    us = best;
+  } else {
+    const tw_status st = api.run_batch(w, batch.total_tokens, prefix, batch.kv_context, m, 0, 0, 2, 0u, &us);
+    if (st != TW_OK) runner_error(api, st, "weavesim: measured iteration");
+  }
   return 1e-6 * static_cast<double>(us) * spec.num_layers;
 }
 

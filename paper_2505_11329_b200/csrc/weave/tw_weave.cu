@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "tw/tw.h"
@@ -91,6 +92,7 @@ struct tw_weave {
   std::vector<double> emu_tokens, emu_fused_us, emu_ar_us;
   int emu_sms = 16;
   int prio_hi = 0;  // greatest stream priority (the boundary stream's)
+  std::map<int64_t, int> tuned_budget;  // tw_weave_throughput's auto boundary budget, per batch size
   void *KV = nullptr, *SC = nullptr, *CO = nullptr;
 };
 
@@ -836,8 +838,35 @@ tw_status tw_weave_throughput(tw_weave_t w, const tw_request* requests, int64_t 
       }
     }
     float us = 0.0f;
-    st = tw_weave_run_batch(w, b.total_tokens, prefix, b.kv_context, m, boundary_sm_budget, gemm_sm_target,
-                            layers_measured, flags, &us);
+    if (m == TW_MODE_WEAVE && boundary_sm_budget == TW_WEAVE_AUTO_BUDGET) {
+      // the boundary budget that schedules best on THIS box: measured once per
+      // batch size over the candidates, then reused (the weave's best budget
+      // differs between boxes and with CUDA-graph replay)
+      auto it = w->tuned_budget.find(b.total_tokens);
+      if (it == w->tuned_budget.end()) {
+        float best = 0.0f;
+        int best_b = 64;
+        for (int cand : {16, 32, 64}) {
+          float t = 0.0f;
+          st = tw_weave_run_batch(w, b.total_tokens, prefix, b.kv_context, m, cand, gemm_sm_target, layers_measured,
+                                  flags, &t);
+          if (st != TW_OK) return st;
+          if (best == 0.0f || t < best) {
+            best = t;
+            best_b = cand;
+          }
+        }
+        w->tuned_budget[b.total_tokens] = best_b;
+        us = best;
+      } else {
+        st = tw_weave_run_batch(w, b.total_tokens, prefix, b.kv_context, m, it->second, gemm_sm_target,
+                                layers_measured, flags, &us);
+      }
+    } else {
+      st = tw_weave_run_batch(w, b.total_tokens, prefix, b.kv_context, m,
+                              boundary_sm_budget == TW_WEAVE_AUTO_BUDGET ? 64 : boundary_sm_budget, gemm_sm_target,
+                              layers_measured, flags, &us);
+    }
     if (st != TW_OK) return st;
     const double lat = 1e-6 * static_cast<double>(us) * num_layers;
     if (iteration_latency_s && k < max_iterations) iteration_latency_s[k] = lat;

@@ -260,9 +260,11 @@ class LayerRunner:
         return us.value
 
     def throughput(self, requests, chunk_size: int, mode: str, num_layers: int = 80, layers_measured: int = 2,
-                   boundary_sms: int = 16, gemm_sms: int = 0, graph: bool = False, threshold: int | None = None):
+                   boundary_sms: int = -1, gemm_sms: int = 0, graph: bool = False, threshold: int | None = None):
         """Measured serving throughput over form_batches(requests, chunk_size)
-        (tw_weave_throughput): a ThroughputResult dict with per-iteration latencies."""
+        (tw_weave_throughput): a ThroughputResult dict with per-iteration latencies.
+        boundary_sms = -1 (TW_WEAVE_AUTO_BUDGET): the weaved batches' fused-op SM
+        budget is measured once per batch size over 16/32/64."""
         reqs = _requests(requests)
         n_iter = len(form_batches(requests, chunk_size))
         lat = (c_double * max(n_iter, 1))()

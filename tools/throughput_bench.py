@@ -37,7 +37,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--tp", type=int, default=8, help="GEMM shapes = one GPU's share at this TP (1 GPU)")
     ap.add_argument("--layers-measured", type=int, default=2)
-    ap.add_argument("--boundary-sms", type=int, default=64)
+    ap.add_argument("--boundary-sms", type=int, default=-1,
+                    help="fused-op SM budget of weaved batches; -1 = measured per batch size over 16/32/64")
     ap.add_argument("--graph", action="store_true", help="time each batch's layers as one CUDA-graph replay")
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--emulate-comm", action="store_true",
@@ -98,7 +99,7 @@ def main():
                 ser = json.load(f)["series"]
             ar = {p["tokens"]: p["microseconds"] for p in ser["allreduce"]}
             r.emulate_comm([p["tokens"] for p in ser["fused"]], [p["microseconds"] for p in ser["fused"]],
-                           [ar[p["tokens"]] for p in ser["fused"]], args.boundary_sms)
+                           [ar[p["tokens"]] for p in ser["fused"]], args.boundary_sms if args.boundary_sms > 0 else 16)
         row = {"name": case["name"], "model": model, "requests": len(reqs),
                "prompt_tokens": sum(p for p, _, _ in reqs), "output_tokens": sum(o for _, o, _ in reqs),
                "chunk_size": case["chunk_size"], "iterations": len(batches),
