@@ -192,6 +192,8 @@ class RefLib:
         L.ref_cmd_throughput_csv.argtypes = [c_char_p, c_char_p, c_int64, c_uint64, c_char_p, c_int64]
         L.ref_cmd_throughput_csv.restype = c_int64
         L.ref_chatlike_trace.argtypes = [c_int64, c_uint64, _I64]
+        L.ref_timeline_json.argtypes = [c_char_p, c_char_p, c_int64, c_char_p, c_char_p, c_int64]
+        L.ref_timeline_json.restype = c_int64
         self.L = L
 
     def rmsnorm_residual(self, inp, res, weight, eps=1e-5):
@@ -353,6 +355,15 @@ class RefLib:
             raise StatusError(9, "ref_cmd_throughput_csv")
         buf = ctypes.create_string_buffer(n + 1)
         self.L.ref_cmd_throughput_csv(model.encode(), profile.encode(), chunk, seed, buf, n + 1)
+        return buf.value.decode()
+
+    def timeline_json(self, profile, model, T, mode) -> str:
+        """The reference's Timeline::to_json of iteration_timeline (modeled)."""
+        n = self.L.ref_timeline_json(profile.encode(), model.encode(), T, mode.encode(), None, 0)
+        if n < 0:
+            raise StatusError(9, "ref_timeline_json")
+        buf = ctypes.create_string_buffer(n + 1)
+        self.L.ref_timeline_json(profile.encode(), model.encode(), T, mode.encode(), buf, n + 1)
         return buf.value.decode()
 
     def chatlike_trace(self, count=96, seed=42):

@@ -424,4 +424,26 @@ int ref_chatlike_trace(std::int64_t count, std::uint64_t seed, std::int64_t* out
   });
 }
 
+// The reference's Timeline JSON (proj/src/scheduler.cpp:301-317) of one
+// iteration_timeline call on a builtin profile / model preset: the schema
+// fixture the measured C++ iteration_timeline is compared with.
+long long ref_timeline_json(const char* profile, const char* model, std::int64_t T, const char* mode, char* buf,
+                            long long cap) {
+  long long n = -1;
+  guarded([&] {
+    const HardwareProfile hp = builtin_profile(profile);
+    const ModelPreset mp = model_preset(model);
+    BatchShape b;
+    b.total_tokens = T;
+    const std::string j = iteration_timeline(b, mp.spec, hp, baseline_mode_from_string(mode), mp.policy).to_json();
+    n = static_cast<long long>(j.size());
+    if (buf && cap > 0) {
+      const long long m = std::min<long long>(n, cap - 1);
+      std::memcpy(buf, j.data(), static_cast<size_t>(m));
+      buf[m] = '\0';
+    }
+  });
+  return n;
+}
+
 }  // extern "C"

@@ -11,6 +11,9 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <vector>
+#include <fstream>
+#include <charconv>
 #include <cstdint>
 #include <string>
 
@@ -37,6 +40,19 @@ const char* to_string(BaselineMode mode) {
     case BaselineMode::NoComm: return "nocomm";
     case BaselineMode::FuseOnly: return "fuseonly";
     case BaselineMode::TokenWeave: return "tokenweave";
+  }
+  return "?";
+}
+
+const char* to_string(OpKind op) {
+  switch (op) {
+    case OpKind::Attention: return "attention";
+    case OpKind::Ffn: return "ffn";
+    case OpKind::FusedARNorm: return "fused_ar_norm";
+    case OpKind::AllReduce: return "allreduce";
+    case OpKind::RmsNorm: return "rmsnorm";
+    case OpKind::AllGatherOp: return "allgather";
+    case OpKind::Misc: return "misc";
   }
   return "?";
 }
@@ -96,6 +112,7 @@ struct WeaveApi {
   decltype(&tw_weave_destroy) destroy = nullptr;
   decltype(&tw_weave_run_batch) run_batch = nullptr;
   decltype(&tw_weave_last_error) last_error = nullptr;
+  decltype(&tw_weave_trace) trace = nullptr;
 };
 
 const WeaveApi& weave_api() {
@@ -113,6 +130,7 @@ const WeaveApi& weave_api() {
     a.destroy = reinterpret_cast<decltype(a.destroy)>(dlsym(h, "tw_weave_destroy"));
     a.run_batch = reinterpret_cast<decltype(a.run_batch)>(dlsym(h, "tw_weave_run_batch"));
     a.last_error = reinterpret_cast<decltype(a.last_error)>(dlsym(h, "tw_weave_last_error"));
+    a.trace = reinterpret_cast<decltype(a.trace)>(dlsym(h, "tw_weave_trace"));
     return a;
   }();
   return api;
@@ -162,45 +180,64 @@ const WeaveApi& require_api() {
   return api;
 }
 
-// One measured iteration: the mode mapping and TokenWeave degrade rules
-// (decode-only and non-Overlap batches run fuse-only, scheduler.cpp:333-341).
-double measured_iteration(const WeaveApi& api, tw_weave_t w, const BatchShape& batch, const LayerSpec& spec,
-                          const HardwareProfile& profile, BaselineMode mode, const SplitPolicy& policy) {
-  tw_weave_mode m = TW_MODE_UNFUSED;
-  std::int64_t prefix = 0;
+// The runner mode and split for a batch: the mode mapping and TokenWeave
+// degrade rules (decode-only and non-Overlap batches run fuse-only,
+// scheduler.cpp:333-341).
+tw_weave_mode runner_mode(const BatchShape& batch, const HardwareProfile& profile, BaselineMode mode,
+                          const SplitPolicy& policy, const SplitPlan* plan_override, std::int64_t* prefix) {
+  *prefix = 0;
   switch (mode) {
     case BaselineMode::Default:
-    case BaselineMode::Multimem: m = TW_MODE_UNFUSED; break;
-    case BaselineMode::NoComm: m = TW_MODE_NO_COMM; break;
-    case BaselineMode::FuseOnly: m = TW_MODE_FUSE_ONLY; break;
-    case BaselineMode::TokenWeave: {
-      m = TW_MODE_FUSE_ONLY;
-      if (!batch.decode_only) {
-        const SplitPlan plan = make_split_plan(batch.total_tokens, profile, policy);
-        if (plan.mode == SplitMode::Overlap && plan.suffix_tokens > 0) {
-          m = TW_MODE_WEAVE;
-          prefix = plan.prefix_tokens;
-        }
-      }
-      break;
-    }
+    case BaselineMode::Multimem: return TW_MODE_UNFUSED;
+    case BaselineMode::NoComm: return TW_MODE_NO_COMM;
+    case BaselineMode::FuseOnly: return TW_MODE_FUSE_ONLY;
+    case BaselineMode::TokenWeave: break;
   }
+  if (batch.decode_only) return TW_MODE_FUSE_ONLY;
+  const SplitPlan plan = plan_override ? *plan_override : make_split_plan(batch.total_tokens, profile, policy);
+  if (plan.mode != SplitMode::Overlap || plan.suffix_tokens <= 0) return TW_MODE_FUSE_ONLY;
+  *prefix = plan.prefix_tokens;
+  return TW_MODE_WEAVE;
+}
+
+// One measured layer of the batch (us).  Weaved layers take the fused op's SM
+// budget that schedules best on this box (16/32/64); `best_budget` reports it.
+float measured_layer_us(const WeaveApi& api, tw_weave_t w, const BatchShape& batch, tw_weave_mode m,
+                        std::int64_t prefix, int* best_budget) {
   float us = 0.0f;
+  *best_budget = 0;
   if (m == TW_MODE_WEAVE) {
-    // the fused op's SM budget that schedules best on this box, over 16/32/64
-    float best = 0.0f;
     for (int cand : {16, 32, 64}) {
       float t = 0.0f;
       const tw_status st = api.run_batch(w, batch.total_tokens, prefix, batch.kv_context, m, cand, 0, 2, 0u, &t);
       if (st != TW_OK) runner_error(api, st, "weavesim: measured iteration");
-      if (best == 0.0f || t < best) best = t;
+      if (us == 0.0f || t < us) {
+        us = t;
+        *best_budget = cand;
+      }
     }
-    us = best;
   } else {
     const tw_status st = api.run_batch(w, batch.total_tokens, prefix, batch.kv_context, m, 0, 0, 2, 0u, &us);
     if (st != TW_OK) runner_error(api, st, "weavesim: measured iteration");
   }
-  return 1e-6 * static_cast<double>(us) * spec.num_layers;
+  return us;
+}
+
+double measured_iteration(const WeaveApi& api, tw_weave_t w, const BatchShape& batch, const LayerSpec& spec,
+                          const HardwareProfile& profile, BaselineMode mode, const SplitPolicy& policy) {
+  std::int64_t prefix = 0;
+  const tw_weave_mode m = runner_mode(batch, profile, mode, policy, nullptr, &prefix);
+  int budget = 0;
+  return 1e-6 * static_cast<double>(measured_layer_us(api, w, batch, m, prefix, &budget)) * spec.num_layers;
+}
+
+// JSON number text: shortest round trip, as nlohmann::json::dump writes it.
+std::string json_number(double v) {
+  char buf[64];
+  auto r = std::to_chars(buf, buf + sizeof(buf), v);
+  std::string s(buf, r.ptr);
+  if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+  return s;
 }
 
 }  // namespace
@@ -213,6 +250,84 @@ double iteration_latency(const BatchShape& batch, const LayerSpec& spec, const H
   if (batch.total_tokens == 0) return 0.0;
   const WeaveApi& api = require_api();
   return measured_iteration(api, runner_for(api, spec, batch.total_tokens), batch, spec, profile, mode, policy);
+}
+
+Timeline iteration_timeline(const BatchShape& batch, const LayerSpec& spec, const HardwareProfile& profile,
+                            BaselineMode mode, const SplitPolicy& policy, const SplitPlan* plan_override) {
+  spec.validate();
+  profile.validate();
+  if (batch.total_tokens < 0 || batch.kv_context < 0) throw DimensionError("iteration_timeline: negative batch shape");
+  Timeline tl;
+  if (batch.total_tokens == 0) return tl;
+  const WeaveApi& api = require_api();
+  if (!api.trace) throw DeviceError("weavesim: libtw_weave.so lacks tw_weave_trace");
+  tw_weave_t w = runner_for(api, spec, batch.total_tokens);
+  std::int64_t prefix = 0;
+  const tw_weave_mode m = runner_mode(batch, profile, mode, policy, plan_override, &prefix);
+  int budget = 0;
+  float us = measured_layer_us(api, w, batch, m, prefix, &budget);
+  if (m == TW_MODE_WEAVE) {  // re-run at the best budget so the trace shows that schedule
+    const tw_status st = api.run_batch(w, batch.total_tokens, prefix, batch.kv_context, m, budget, 0, 2, 0u, &us);
+    if (st != TW_OK) runner_error(api, st, "weavesim: measured iteration");
+  }
+  int n = 0;
+  int op[16], sp[16], stm[16];
+  float a[16], b[16];
+  const tw_status st = api.trace(w, 16, &n, op, sp, stm, a, b);
+  if (st != TW_OK) runner_error(api, st, "weavesim: trace");
+  float t0 = n ? a[0] : 0.0f;
+  for (int i = 0; i < n; ++i) t0 = std::min(t0, a[i]);
+  for (int i = 0; i < n; ++i) {
+    StreamEvent e;
+    e.id = i;
+    e.op = op[i] == TW_OP_ATTENTION ? OpKind::Attention : op[i] == TW_OP_FFN ? OpKind::Ffn : OpKind::FusedARNorm;
+    e.split = sp[i] == 0 ? SplitId::Prefix : sp[i] == 1 ? SplitId::Suffix : SplitId::Whole;
+    // the reference's DAG puts every collective on the comm stream, sequential
+    // modes included (ordered by edges); the runner serialises those on the
+    // compute stream, so the label follows the op
+    e.stream = (stm[i] || e.op == OpKind::FusedARNorm) ? StreamId::Comm : StreamId::Compute;
+    // the DAG edges of build_layer_graph (scheduler.cpp:119-147 weave, :150-181 chains)
+    if (n == 8) {
+      static const std::vector<int> deps[8] = {{}, {0}, {0}, {2, 1}, {1}, {4, 3}, {3}, {6, 5}};
+      e.depends_on = deps[i];
+    } else if (i > 0) {
+      e.depends_on = {i - 1};
+    }
+    e.start = 1e-6 * static_cast<double>(a[i] - t0);
+    e.end = 1e-6 * static_cast<double>(b[i] - t0);
+    tl.events.push_back(e);
+  }
+  tl.iteration_latency = 1e-6 * static_cast<double>(us) * spec.num_layers;
+  return tl;
+}
+
+std::string Timeline::to_json() const {
+  // the reference's Timeline::to_json layout (json dump(2): sorted keys,
+  // two-space indent, id lists inline)
+  std::string o = "{\n  \"events\": [";
+  for (size_t i = 0; i < events.size(); ++i) {
+    const StreamEvent& e = events[i];
+    o += i ? ",\n    {\n" : "\n    {\n";
+    o += "      \"depends_on\": [";  // the reference build prints id lists inline: [2,1]
+    for (size_t k = 0; k < e.depends_on.size(); ++k) o += (k ? "," : "") + std::to_string(e.depends_on[k]);
+    o += "],\n";
+    o += "      \"end\": " + json_number(e.end) + ",\n";
+    o += "      \"id\": " + std::to_string(e.id) + ",\n";
+    o += std::string("      \"op\": \"") + to_string(e.op) + "\",\n";
+    o += std::string("      \"split\": \"") +
+         (e.split == SplitId::Prefix ? "prefix" : e.split == SplitId::Suffix ? "suffix" : "whole") + "\",\n";
+    o += "      \"start\": " + json_number(e.start) + ",\n";
+    o += std::string("      \"stream\": \"") + (e.stream == StreamId::Comm ? "comm" : "compute") + "\"\n    }";
+  }
+  o += events.empty() ? "],\n" : "\n  ],\n";
+  o += "  \"iteration_latency\": " + json_number(iteration_latency) + "\n}";
+  return o;
+}
+
+void Timeline::to_json_file(const std::string& path) const {
+  std::ofstream out(path);
+  if (!out) throw ParseError("cannot write timeline: " + path);
+  out << to_json() << "\n";
 }
 
 ThroughputResult simulate_throughput(const std::vector<Request>& requests, const LayerSpec& spec,

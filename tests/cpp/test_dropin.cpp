@@ -427,7 +427,21 @@ void throughput_gpu_cases() {
 
 }  // namespace
 
-// usage: test_dropin host | gpu | acceptance
+// test_dropin timeline <dir>: the measured iteration_timeline JSON of one
+// Llama-3.3-70B layer (T = 8192, TP = 8 shapes) for TokenWeave and FuseOnly,
+// written to <dir>/timeline_<mode>.json (schema-checked by tests/test_dropin.py).
+void timeline_cases(const std::string& dir) {
+  const ModelPreset preset = model_preset("llama-70b");
+  BatchShape b;
+  b.total_tokens = 8192;
+  for (BaselineMode m : {BaselineMode::TokenWeave, BaselineMode::FuseOnly}) {
+    const Timeline t = iteration_timeline(b, preset.spec, builtin_profile("b200"), m, preset.policy);
+    CHECK(!t.events.empty() && t.iteration_latency > 0);
+    t.to_json_file(dir + "/timeline_" + to_string(m) + ".json");
+  }
+}
+
+// usage: test_dropin host | gpu | acceptance | timeline <dir>
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "host";
   host_cases();
@@ -438,6 +452,7 @@ int main(int argc, char** argv) {
     acceptance_cases(false);
   }
   if (mode == "acceptance") acceptance_cases(true);
+  if (mode == "timeline") timeline_cases(argc > 2 ? argv[2] : ".");
   std::printf("%s: %d passed, %d failed\n", mode.c_str(), g_pass, g_fail);
   return g_fail ? 1 : 0;
 }

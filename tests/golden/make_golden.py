@@ -145,6 +145,9 @@ def main() -> None:
             row[mode] = ref.simulate_throughput("b200", model, mode, reqs, chunk)
         meta["throughput_pred"].append(row)
     meta["cli_throughput_csv"] = ref.cmd_throughput_csv("llama-70b", "b200", 2048, 42)
+    # Timeline JSON schema fixture (modeled values; the measured C++ timeline
+    # must produce the same keys, vocabularies and DAG edges per layer)
+    meta["timeline_json"] = {m: ref.timeline_json("b200", "llama-70b", 8192, m) for m in ("tokenweave", "fuseonly")}
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=1)
