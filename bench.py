@@ -30,6 +30,13 @@ import sys
 import threading
 import time
 
+ROOT_DIR = os.path.dirname(os.path.abspath(__file__))
+if ROOT_DIR not in sys.path:
+    sys.path.insert(0, ROOT_DIR)
+# our libraries (and the CUDA toolkit's cuBLAS the weave runner is built
+# against) load before torch does -- see paper_2505_11329_b200/_lib.py
+import paper_2505_11329_b200  # noqa: E402,F401
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -368,6 +375,7 @@ def run_ours_single(args):
                 "tokenweave": round(min(r.run(T, "tokenweave", prefix=a, boundary_sms=b, layers=6)
                                         for b in (16, 32, 64)), 1),
                 "nocomm": round(r.run(T, "nocomm", layers=6), 1),
+                "cublas_version": r.cublas_version,
                 "note": "per-layer device time, eager launches; GEMMs are cuBLAS load (not product)"}
             r.close()
         except Exception as exc:  # libtw_weave / cuBLAS unavailable: report, do not fail the bench

@@ -55,6 +55,10 @@ typedef struct tw_weave* tw_weave_t;
 
 /* Message of the last failing call of this header on this thread ("" if none). */
 TW_API const char* tw_weave_last_error(void);
+/* Version of the cuBLAS the runner's GEMMs actually bind (e.g. 120901 = 12.9.1;
+ * 0 without a device).  The process may hold another libcublas.so.12 (torch's)
+ * loaded first; DESIGN.md §5. */
+TW_API int tw_weave_cublas_version(void);
 
 TW_API tw_status tw_weave_create(const tw_layer_spec* spec, int64_t max_tokens, int device, tw_weave_t* out);
 /* TP >= 2 with one process per GPU: `comm` is a multi-process communicator

@@ -106,7 +106,29 @@ _SIGNATURES = [
 ]
 
 
+def _preload_cuda_cublas() -> None:
+    """Bind the CUDA toolkit's cuBLAS (12.9, the one libtw_weave.so is built
+    against) before anything else loads a libcublas.so.12: torch ships its own
+    (12.8) and, loaded first, would serve the weave runner's GEMMs too -- with
+    different kernel choices (the weave measured 1673 vs 1328 us per layer at
+    Llama TP=8 shapes, T=8192).  A later `import torch` then
+    reuses the already-loaded libraries (same SONAME).  No-op if torch's
+    copy is already in the process or the toolkit is absent."""
+    import sys
+    if "torch" in sys.modules:
+        return
+    root = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    for name in ("libcublasLt.so.12", "libcublas.so.12"):
+        path = os.path.join(root, "lib64", name)
+        if os.path.exists(path):
+            try:
+                ctypes.CDLL(path, mode=ctypes.RTLD_GLOBAL)
+            except OSError:
+                return
+
+
 def _load() -> ctypes.CDLL:
+    _preload_cuda_cublas()
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} not built: run `make lib` (or __graft_entry__.build()); "
                           "there is no CPU fallback for the TokenWeave path")

@@ -402,6 +402,16 @@ extern "C" {
 
 const char* tw_weave_last_error(void) { return g_err; }
 
+int tw_weave_cublas_version(void) {
+  int v = 0;
+  cublasHandle_t h = nullptr;
+  if (cublasCreate(&h) == CUBLAS_STATUS_SUCCESS) {
+    cublasGetVersion(h, &v);
+    cublasDestroy(h);
+  }
+  return v;
+}
+
 tw_status tw_weave_emulate_comm(tw_weave_t w, const int64_t* tokens, const float* fused_us, const float* allreduce_us,
                                 int n, int sms) {
   if (!w) return werr(TW_ERR_CONFIG, "weave_emulate_comm: null runner");

@@ -199,6 +199,8 @@ def _weave_lib():
     lib.tw_weave_emulate_comm.argtypes = [c_void_p, POINTER(c_int64), POINTER(c_float), POINTER(c_float), c_int,
                                           c_int]
     lib.tw_weave_emulate_comm.restype = c_int
+    lib.tw_weave_cublas_version.restype = c_int
+    lib.tw_weave_cublas_version.argtypes = []
     lib.tw_weave_last_error.restype = ctypes.c_char_p
     lib.tw_weave_last_error.argtypes = []
     lib.tw_weave_trace.argtypes = [c_void_p, c_int, POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_int),
@@ -227,6 +229,11 @@ class LayerRunner:
         else:
             self._check(self._L.tw_weave_create(ctypes.byref(self.spec), max_tokens, device, ctypes.byref(h)))
         self._h = h
+
+    @property
+    def cublas_version(self) -> int:
+        """The cuBLAS version the runner's GEMMs bind (e.g. 120901)."""
+        return int(self._L.tw_weave_cublas_version())
 
     def _check(self, status: int) -> None:
         check(status, self._L.tw_weave_last_error)

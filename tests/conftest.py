@@ -9,6 +9,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+# Load our libraries (and with them the CUDA toolkit's cuBLAS) before any test
+# imports torch, so the weave runner binds the cuBLAS it is built against.
+import paper_2505_11329_b200  # noqa: E402,F401
+
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA B200 (run with -m gpu on the GPU box)")

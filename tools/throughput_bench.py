@@ -94,6 +94,7 @@ def main():
             comm = h
             kw["comm"] = h
         r = weave.LayerRunner(model, tp=tp, max_tokens=max_t, **kw)
+        res["cublas_version"] = r.cublas_version
         if args.emulate_comm:
             with open(os.path.join(ROOT, "profiles", "microbench_b200_measured.json")) as f:
                 ser = json.load(f)["series"]

@@ -153,6 +153,7 @@ def main():
            "layers_timed": args.layers, "rows": []}
     for model, tp, tokens, budgets in cases:
         r = weave.LayerRunner(model, tp=tp, max_tokens=max(tokens))
+        res["cublas_version"] = r.cublas_version
         for T in tokens:
             row = bench_case(weave, r, T, args.layers, budgets, ref, model, tp)
             res["rows"].append(row)

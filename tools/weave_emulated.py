@@ -42,6 +42,7 @@ def main():
     for model, tokens in (("llama-70b", [1024, 2048, 4096, 8192]), ("mixtral-8x22b", [4096, 8192]),
                           ("qwen-72b", [256, 512, 1024, 2048, 4096, 8192, 16384])):
         r = weave.LayerRunner(model, tp=8, max_tokens=max(tokens))
+        res["cublas_version"] = r.cublas_version
         r.emulate_comm(toks, fused, ar, args.sms)
         for T in tokens:
             a, b, off, mode = weave.make_split_plan(T, threshold=r.threshold)
