@@ -1,4 +1,6 @@
-"""Weave timing stability check, optionally after other work in the same
+"""Weave timing stability check (imports torch FIRST, so the runner binds
+torch's bundled cuBLAS 12.8 unless the package was loaded earlier -- compare
+tools/weave_repeat_notorch.py, which binds the toolkit's 12.9), optionally after other work in the same
 process (argv[1]: 'k1' = co-located K1 first, 'k2' = big K2 first, 'tp1' = a
 TP=1-shape runner created, run and freed first, 'allocN' = N GB allocated and
 freed first)."""
