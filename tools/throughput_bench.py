@@ -25,6 +25,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+# before torch: the layer runner binds the CUDA toolkit's cuBLAS (see _lib.py)
+import paper_2505_11329_b200  # noqa: E402,F401
 
 NUM_LAYERS = {"llama-70b": 80, "qwen-72b": 80, "mixtral-8x22b": 56}  # proj/src/presets.cpp:72-97
 MODES = ("unfused", "fuseonly", "tokenweave", "nocomm")

@@ -17,6 +17,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+# before torch: the layer runner binds the CUDA toolkit's cuBLAS (see _lib.py)
+import paper_2505_11329_b200  # noqa: E402,F401
 
 
 def main():
