@@ -688,7 +688,18 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
   const int dev0 = comm->ranks[comm->local_rank < 0 ? 0 : comm->local_rank].device;
   cudaSetDevice(dev0);
   const int sms = sm_count(dev0);
-  if (fused) {
+  // PEER with a small world (W <= 4): the bulk-copy pipeline
+  // (tw_peer_tma.cuh) whenever the shape fits -- simulated ranks on one B200,
+  // T = 8192 x H = 8192: TP = 2 141 vs 182 us, TP = 4 266 vs 279 us
+  // (tools/k1_peer_ab.sh).  TW_K1_PEER_ENGINE=rows forces the row engine.
+  static const char* peer_env = std::getenv("TW_K1_PEER_ENGINE");
+  int peer_tma_bpsm = 0;
+  if (fused && !nvls && vec && W <= kPeerTmaMaxWorld && !(peer_env && std::strcmp(peer_env, "rows") == 0))
+    peer_tma_bpsm = k1_peer_tma_blocks_per_sm(W, static_cast<int>(H / nv), H, bf16);
+  if (peer_tma_bpsm > 0) {
+    const int slots = comm->colocated ? W : 1;
+    budget = std::min(budget, std::max(1, sms * peer_tma_bpsm / slots));
+  } else if (fused) {
     const int bpsm = std::max(1, rownorm_blocks_per_sm(plan, bf16, x));
     const int slots = comm->colocated ? W : 1;
     // Every CTA of every co-launched rank must be resident for the barrier.
@@ -729,6 +740,7 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
     s.gen = comm->ranks[r].gen;
   };
   auto launch = [&](const RowParams& pp, dim3 grid, cudaStream_t s) {
+    if (peer_tma_bpsm > 0) return launch_k1_peer_tma(pp, W, static_cast<int>(H / nv), bf16, grid, s);
     return fused ? launch_rownorm(pp, plan, bf16, x, grid, s) : launch_allreduce(pp, plan, bf16, x, grid, s);
   };
   if (comm->colocated) {

@@ -244,4 +244,72 @@ cudaError_t launch_count_nonfinite(const void* x, long long n, bool bf16, int* c
   return cudaGetLastError();
 }
 
+// ---- K1 over PEER as a bulk-copy pipeline ---------------------------------------------
+
+namespace {
+using PeerTmaFn = void (*)(RowParams);
+
+template <class E, int W>
+PeerTmaFn pick_peer_tma_w(int vpt) {
+  vpt = vpt <= 1 ? 1 : vpt <= 2 ? 2 : vpt <= 4 ? 4 : 0;  // c < V guards the rest
+  switch (vpt) {
+    case 1: return k1_peer_tma_kernel<E, 1, W>;
+    case 2: return k1_peer_tma_kernel<E, 2, W>;
+    case 4: return k1_peer_tma_kernel<E, 4, W>;
+    default: return nullptr;
+  }
+}
+
+template <class E>
+PeerTmaFn pick_peer_tma(int world, int vpt) {
+  switch (world) {
+    case 2: return pick_peer_tma_w<E, 2>(vpt);
+    case 3: return pick_peer_tma_w<E, 3>(vpt);
+    case 4: return pick_peer_tma_w<E, 4>(vpt);
+    default: return nullptr;
+  }
+}
+
+// Ring depth and shared-memory bytes for (W+1)-row stages under a 200 KB budget.
+bool peer_tma_geometry(int world, long long H, bool bf16, int* stages, size_t* smem) {
+  const size_t row = static_cast<size_t>(H) * (bf16 ? 2 : 4);
+  const size_t stage = (world + 1) * row;
+  const int S = static_cast<int>(std::min<size_t>(4, (200 * 1024) / stage));
+  if (S < 2) return false;
+  *stages = S;
+  *smem = S * stage + 2 * S * sizeof(uint64_t) + 2 * 8 * sizeof(double);
+  return true;
+}
+}  // namespace
+
+int k1_peer_tma_blocks_per_sm(int world, int V, long long H, bool bf16) {
+  const int vpt = (V + 255) / 256;
+  PeerTmaFn fn = bf16 ? pick_peer_tma<uint16_t>(world, vpt) : pick_peer_tma<float>(world, vpt);
+  int S = 0;
+  size_t smem = 0;
+  if (!fn || !peer_tma_geometry(world, H, bf16, &S, &smem)) return 0;
+  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(smem)) != cudaSuccess)
+    return 0;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reinterpret_cast<const void*>(fn), 288, smem) != cudaSuccess)
+    return 0;
+  return n;
+}
+
+cudaError_t launch_k1_peer_tma(RowParams params, int world, int V, bool bf16, dim3 grid, cudaStream_t stream) {
+  const int vpt = (V + 255) / 256;
+  PeerTmaFn fn = bf16 ? pick_peer_tma<uint16_t>(world, vpt) : pick_peer_tma<float>(world, vpt);
+  int S = 0;
+  size_t smem = 0;
+  if (!fn || !peer_tma_geometry(world, params.H, bf16, &S, &smem)) return cudaErrorNotSupported;
+  cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  params.V = V;
+  params.nslots_stages = S;
+  void* args[] = {&params};
+  return cudaLaunchKernel(reinterpret_cast<const void*>(fn), grid, dim3(288), args, smem, stream);
+}
+
 }  // namespace tw

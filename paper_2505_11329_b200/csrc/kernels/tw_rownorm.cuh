@@ -80,6 +80,7 @@ struct RowParams {
   int* err;
   long long spin_limit;   // barrier poll bound before the timeout flag is raised
   int drop_arrival_rank;  // fault injection (tests): this rank never signals; -1 = none
+  int nslots_stages;      // k1_peer_tma_kernel: smem ring depth
 };
 
 constexpr unsigned kGatherResidual = 0x1u;
