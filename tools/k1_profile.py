@@ -1,5 +1,6 @@
-"""One K1 launch (8 simulated ranks, PEER, T=1024 x H=8192 bf16, whole GPU)
-for ncu: `ncu --set full -k regex:rownorm_kernel -c 1 python tools/k1_profile.py`."""
+"""K1 launches (W simulated ranks, PEER, T x H=8192 bf16, whole GPU) for ncu:
+`ncu --set full -k regex:rownorm_kernel -c 1 python tools/k1_profile.py [W] [T]`
+(W <= 4 runs the bulk-copy engine: `-k regex:k1_peer_tma`)."""
 import os
 import sys
 
@@ -9,7 +10,9 @@ import torch  # noqa: E402
 
 import paper_2505_11329_b200 as tw  # noqa: E402
 
-W, T, H = 8, 1024, 8192
+W = int(sys.argv[1]) if len(sys.argv) > 1 else 8   # W <= 4: the PEER bulk-copy engine
+T = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
+H = 8192
 comm = tw.Communicator(W, [0] * W, T * H * 2, tw.TW_TRANSPORT_PEER)
 for q in range(W):
     comm.buffer(q, tw.TW_BUF_INPUT, (T, H), torch.bfloat16).normal_()
