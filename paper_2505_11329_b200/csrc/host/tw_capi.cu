@@ -688,10 +688,10 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
   const int dev0 = comm->ranks[comm->local_rank < 0 ? 0 : comm->local_rank].device;
   cudaSetDevice(dev0);
   const int sms = sm_count(dev0);
-  // PEER with a small world (W <= 4): the bulk-copy pipeline
-  // (tw_peer_tma.cuh) whenever the shape fits -- simulated ranks on one B200,
-  // T = 8192 x H = 8192: TP = 2 141 vs 182 us, TP = 4 266 vs 279 us
-  // (tools/k1_peer_ab.sh).  TW_K1_PEER_ENGINE=rows forces the row engine.
+  // PEER: the bulk-copy pipeline (tw_peer_tma.cuh) whenever the shape fits
+  // its ring -- simulated ranks on one B200, T = 8192 x H = 8192: TP = 2
+  // 141 vs 182 us, TP = 4 266 vs 279 us (tools/k1_peer_ab.sh).
+  // TW_K1_PEER_ENGINE=rows forces the row engine.
   static const char* peer_env = std::getenv("TW_K1_PEER_ENGINE");
   int peer_tma_bpsm = 0;
   if (fused && !nvls && vec && W <= kPeerTmaMaxWorld && !(peer_env && std::strcmp(peer_env, "rows") == 0))

@@ -260,20 +260,23 @@ PeerTmaFn pick_peer_tma_w(int vpt) {
   }
 }
 
+// Worlds 2, 3, 4 (one stage per row) and 8 (two); others use the row engine.
 template <class E>
 PeerTmaFn pick_peer_tma(int world, int vpt) {
   switch (world) {
     case 2: return pick_peer_tma_w<E, 2>(vpt);
     case 3: return pick_peer_tma_w<E, 3>(vpt);
     case 4: return pick_peer_tma_w<E, 4>(vpt);
+    case 8: return pick_peer_tma_w<E, 8>(vpt);
     default: return nullptr;
   }
 }
 
-// Ring depth and shared-memory bytes for (W+1)-row stages under a 200 KB budget.
+// Ring depth under a 200 KB shared-memory budget: peer_tma_stage_rows(W)
+// rows per stage, 2..4 stages (0 = the shape does not fit).
 bool peer_tma_geometry(int world, long long H, bool bf16, int* stages, size_t* smem) {
   const size_t row = static_cast<size_t>(H) * (bf16 ? 2 : 4);
-  const size_t stage = (world + 1) * row;
+  const size_t stage = peer_tma_stage_rows(world) * row;
   const int S = static_cast<int>(std::min<size_t>(4, (200 * 1024) / stage));
   if (S < 2) return false;
   *stages = S;
@@ -291,10 +294,10 @@ int k1_peer_tma_blocks_per_sm(int world, int V, long long H, bool bf16) {
   if (cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                            static_cast<int>(smem)) != cudaSuccess)
     return 0;
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reinterpret_cast<const void*>(fn), 288, smem) != cudaSuccess)
+  int b = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, reinterpret_cast<const void*>(fn), 288, smem) != cudaSuccess)
     return 0;
-  return n;
+  return b;
 }
 
 cudaError_t launch_k1_peer_tma(RowParams params, int world, int V, bool bf16, dim3 grid, cudaStream_t stream) {
@@ -308,6 +311,7 @@ cudaError_t launch_k1_peer_tma(RowParams params, int world, int V, bool bf16, di
   if (e != cudaSuccess) return e;
   params.V = V;
   params.nslots_stages = S;
+  params.world = world;
   void* args[] = {&params};
   return cudaLaunchKernel(reinterpret_cast<const void*>(fn), grid, dim3(288), args, smem, stream);
 }

@@ -29,9 +29,9 @@ cudaError_t launch_rownorm(const RowParams& params, const RowPlan& plan, bool bf
 cudaError_t launch_allreduce(const RowParams& params, const RowPlan& plan, bool bf16, Xport x, dim3 grid,
                              cudaStream_t stream);
 int rownorm_blocks_per_sm(const RowPlan& plan, bool bf16, Xport x);
-// K1 over PEER as a bulk-copy pipeline (tw_peer_tma.cuh), world <= 4, vectorised
-// rows.  Returns cudaErrorNotSupported when the shape does not fit (the caller
-// falls back to the row engine); *ctas_per_sm reports co-residency.
+// K1 over PEER as a bulk-copy pipeline (tw_peer_tma.cuh), 2 <= world <= 8,
+// vectorised rows.  Returns cudaErrorNotSupported when the shape does not fit;
+// k1_peer_tma_blocks_per_sm returns 0 then (the caller uses the row engine).
 cudaError_t launch_k1_peer_tma(RowParams params, int world, int V, bool bf16, dim3 grid, cudaStream_t stream);
 int k1_peer_tma_blocks_per_sm(int world, int V, long long H, bool bf16);
 size_t bulk_smem_bytes(int stages, uint32_t row_bytes, int tpr, int groups);

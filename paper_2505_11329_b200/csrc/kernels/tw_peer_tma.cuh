@@ -1,14 +1,21 @@
 // tw_peer_tma.cuh -- K1 over the PEER transport as a bulk-copy pipeline (the
-// K2 TMA engine's structure, tw_bulk.cuh) for small worlds (W <= 4).
+// K2 TMA engine's structure, tw_bulk.cuh).
 //
-// Per owned token row: the producer thread bulk-loads the W ranks' INPUT rows
-// and this rank's residual row into one ring stage ((W+1) rows); 256 consumer
-// threads sum the W partial rows in rank-ascending fp32 order from 0.0f (the
-// reference's order, proj/src/collectives.cpp:74-78, so residuals stay
-// bitwise), add the residual, write r' over the residual slot and the normed
-// output over slot 0, and the storer thread bulk-stores r' to the local shard,
-// the output to every rank's OUTPUT (and r' to every rank's RESIDUAL with
-// G = 2).  The rank barriers are the row engine's (tw_rownorm.cuh).
+// Per owned token row the producer thread bulk-loads W + 1 rows -- the W
+// ranks' INPUT rows in rank order, then this rank's residual row -- into
+// `nchunks` consecutive ring stages (the W + 1 loads split evenly, the larger
+// chunks last, so the final stage holds the residual and at least one input
+// row).  256 consumer threads sum the W partial rows in rank-ascending fp32
+// order from 0.0f in registers across the chunks (the reference's order,
+// proj/src/collectives.cpp:74-78, so residuals stay bitwise), add the
+// residual, write r' over the residual slot and the normed output over slot 0
+// of the final stage, and the storer thread bulk-stores r' to the local
+// shard, the output to every rank's OUTPUT (and r' to every rank's RESIDUAL
+// with G = 2).  W <= 4 takes one stage per row; W = 8 splits a row over two
+// stages (4 + 5 rows) so the ring still double-buffers inside the shared-
+// memory budget.  W and the chunking are compile-time, so every per-stage
+// sum is unrolled and its shared-memory loads issue together.  The rank
+// barriers are the row engine's (tw_rownorm.cuh).
 #pragma once
 
 #include "tw_bulk.cuh"
@@ -16,31 +23,43 @@
 
 namespace tw {
 
-constexpr int kPeerTmaMaxWorld = 4;
+constexpr int kPeerTmaMaxWorld = kMaxRanks;
+__host__ __device__ constexpr int peer_tma_chunks(int W) { return W <= 4 ? 1 : 2; }
+__host__ __device__ constexpr int peer_tma_stage_rows(int W) {
+  return (W + 1 + peer_tma_chunks(W) - 1) / peer_tma_chunks(W);
+}
 
 template <class E, int VPT, int W>
 __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_constant__ RowParams p) {
   constexpr int N = 16 / sizeof(E);
   using VT = Vec<E, N>;
   using Acc = typename std::conditional<sizeof(E) == 4, double, float>::type;
+  constexpr int tpr = 256;
+  constexpr int cwarps = tpr / 32;
   extern __shared__ __align__(128) unsigned char smem[];
   const RankSlot& s = p.slot[blockIdx.y];
-  const int S = p.nslots_stages;  // ring depth
+  const int S = p.nslots_stages;  // ring depth (stages)
+  constexpr int n = peer_tma_chunks(W);  // stages per row
+  constexpr int tot = W + 1;             // row loads per token: W inputs + the residual
+  constexpr int base = tot / n, extra = tot % n;
+  constexpr int R = peer_tma_stage_rows(W);  // rows per stage (the last chunk is the largest)
   const uint32_t row_bytes = static_cast<uint32_t>(p.H * sizeof(E));
-  const size_t stage_bytes = static_cast<size_t>(W + 1) * row_bytes;
-  unsigned char* ring = smem;  // [S][W inputs | residual]
+  const size_t stage_bytes = static_cast<size_t>(R) * row_bytes;
+  // With more stages than chunks the final stage of a row is released one row
+  // late (after the next row's stores are issued); otherwise that would block
+  // the producer's next row, so the storer waits for its own reads instead.
+  const bool lazy = S > n;
+  unsigned char* ring = smem;  // [S][R rows]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(S) * stage_bytes);
   uint64_t* empty = full + S;
   Acc* part = reinterpret_cast<Acc*>(empty + S);  // [2][8 consumer warps]
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  constexpr int tpr = 256;
-  constexpr int cwarps = tpr / 32;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], cwarps);
     }
     mbar_fence_init();
   }
@@ -52,20 +71,25 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
 
   if (warp == 0) {
     if (lane == 0) {
+      long long g = 0;  // stage sequence number
       for (long long i = 0; i < nrows; ++i) {
-        const int st = static_cast<int>(i % S);
-        const uint32_t ph = static_cast<uint32_t>((i / S) & 1);
-        if (i >= S) mbar_wait(&empty[st], ph ^ 1u);
         const long long t = row0 + blockIdx.x + i * stride;
-        unsigned char* dst = ring + static_cast<size_t>(st) * stage_bytes;
-        mbar_arrive_expect_tx(&full[st], (W + 1) * row_bytes);
+        int item = 0;
 #pragma unroll
-        for (int q = 0; q < W; ++q)
-          bulk_g2s(dst + q * row_bytes,
-                   static_cast<const unsigned char*>(p.peer_in[q]) + (p.row_offset + t) * row_bytes, row_bytes,
-                   &full[st]);
-        bulk_g2s(dst + W * row_bytes, static_cast<const unsigned char*>(s.residual) + (t - row0) * row_bytes,
-                 row_bytes, &full[st]);
+        for (int c = 0; c < n; ++c, ++g) {
+          const int cnt = base + (c >= n - extra ? 1 : 0);
+          const int st = static_cast<int>(g % S);
+          if (g >= S) mbar_wait(&empty[st], static_cast<uint32_t>(((g / S) & 1) ^ 1));
+          unsigned char* dst = ring + static_cast<size_t>(st) * stage_bytes;
+          mbar_arrive_expect_tx(&full[st], cnt * row_bytes);
+#pragma unroll
+          for (int k = 0; k < cnt; ++k, ++item) {
+            const unsigned char* src =
+                item < W ? static_cast<const unsigned char*>(p.peer_in[item]) + (p.row_offset + t) * row_bytes
+                         : static_cast<const unsigned char*>(s.residual) + (t - row0) * row_bytes;
+            bulk_g2s(dst + k * row_bytes, src, row_bytes, &full[st]);
+          }
+        }
       }
     }
   } else {
@@ -78,55 +102,88 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
       const int c = lt + k * tpr;
       if (c < p.V) load_weight<N>(s.weight, static_cast<long long>(c) * N, w[k]);
     }
+    long long g = 0;
+    int prev_last = -1;  // final stage of the previous row (lazy release)
     for (long long i = 0; i < nrows; ++i) {
-      const int st = static_cast<int>(i % S);
-      const uint32_t ph = static_cast<uint32_t>((i / S) & 1);
       const long long t = row0 + blockIdx.x + i * stride;
+      float x[VPT][N];
+#pragma unroll
+      for (int k = 0; k < VPT; ++k)
+#pragma unroll
+        for (int j = 0; j < N; ++j) x[k][j] = 0.0f;
+      // Every chunk but the last holds input rows only: sum, release.
+#pragma unroll
+      for (int c = 0; c < n - 1; ++c, ++g) {
+        const int cnt = base + (c >= n - extra ? 1 : 0);
+        const int st = static_cast<int>(g % S);
+        mbar_wait(&full[st], static_cast<uint32_t>((g / S) & 1));
+        const unsigned char* stg = ring + static_cast<size_t>(st) * stage_bytes;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+          const int cc = lt + k * tpr;
+          if (cc < p.V) {
+#pragma unroll
+            for (int q = 0; q < cnt; ++q) {  // rank-ascending fp32 sum from 0.0f
+              float f[N];
+              VT::unpack(lds_v4(stg + q * row_bytes + cc * 16), f);
+#pragma unroll
+              for (int j = 0; j < N; ++j) x[k][j] += f[j];
+            }
+          }
+        }
+      }
+      // The last chunk: the remaining inputs, then the residual row.
+      constexpr int cnt = base + (extra ? 1 : 0);
+      const int st = static_cast<int>(g % S);
+      mbar_wait(&full[st], static_cast<uint32_t>((g / S) & 1));
+      ++g;
       unsigned char* stg = ring + static_cast<size_t>(st) * stage_bytes;
-      unsigned char* res = stg + W * row_bytes;
-      mbar_wait(&full[st], ph);
+      unsigned char* res = stg + (cnt - 1) * row_bytes;
       typename VT::Raw rr[VPT];
       Acc ss = 0;
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
-        const int c = lt + k * tpr;
-        if (c < p.V) {
-          float x[N], r[N];
+        const int cc = lt + k * tpr;
+        if (cc < p.V) {
 #pragma unroll
-          for (int j = 0; j < N; ++j) x[j] = 0.0f;
-#pragma unroll
-          for (int q = 0; q < W; ++q) {  // rank-ascending fp32 sum from 0.0f
+          for (int q = 0; q < cnt - 1; ++q) {
             float f[N];
-            VT::unpack(lds_v4(stg + q * row_bytes + c * 16), f);
+            VT::unpack(lds_v4(stg + q * row_bytes + cc * 16), f);
 #pragma unroll
-            for (int j = 0; j < N; ++j) x[j] += f[j];
+            for (int j = 0; j < N; ++j) x[k][j] += f[j];
           }
-          VT::unpack(lds_v4(res + c * 16), r);
+          float r[N];
+          VT::unpack(lds_v4(res + cc * 16), r);
 #pragma unroll
-          for (int j = 0; j < N; ++j) r[j] = x[j] + r[j];
+          for (int j = 0; j < N; ++j) r[j] = x[k][j] + r[j];
           rr[k] = VT::pack(r);
           VT::unpack(rr[k], r);
 #pragma unroll
           for (int j = 0; j < N; ++j) ss += static_cast<Acc>(r[j]) * static_cast<Acc>(r[j]);
-          sts_v4(res + c * 16, rr[k]);  // r' over the residual slot
+          sts_v4(res + cc * 16, rr[k]);  // r' over the residual slot
         }
       }
       ss = warp_sum(ss);
       Acc* pp = part + (i & 1) * cwarps;
       if (lane == 0) pp[cw] = ss;
       named_bar_sync(1, tpr);
+      // Every consumer is past the input-only stages of this row: free them.
+      if (storer) {
+#pragma unroll
+        for (int c = 0; c < n - 1; ++c) mbar_arrive_n(&empty[static_cast<int>((g - n + c) % S)], cwarps);
+      }
       Acc total = 0;
       for (int q = 0; q < cwarps; ++q) total += pp[q];
       const float inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(p.H)) + p.eps);
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
-        const int c = lt + k * tpr;
-        if (c < p.V) {
+        const int cc = lt + k * tpr;
+        if (cc < p.V) {
           float o[N];
           VT::unpack(rr[k], o);
 #pragma unroll
           for (int j = 0; j < N; ++j) o[j] = o[j] * inv * w[k][j];
-          sts_v4(stg + c * 16, VT::pack(o));  // output over input slot 0
+          sts_v4(stg + cc * 16, VT::pack(o));  // output over input slot 0
         }
       }
       fence_proxy_async_smem();
@@ -140,9 +197,15 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
           if (p.flags & kGatherResidual) bulk_s2g(static_cast<unsigned char*>(p.peer_res[q]) + grow, res, row_bytes);
         }
         bulk_commit();
-        if (i > 0) {
-          bulk_wait_read<1>();
-          mbar_arrive(&empty[(i - 1) % S]);
+        if (lazy) {
+          if (prev_last >= 0) {
+            bulk_wait_read<1>();
+            mbar_arrive_n(&empty[prev_last], cwarps);
+          }
+          prev_last = st;
+        } else {
+          bulk_wait_read<0>();
+          mbar_arrive_n(&empty[st], cwarps);
         }
       }
     }

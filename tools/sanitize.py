@@ -1,5 +1,5 @@
 """Small K1/K2/K3 launches for compute-sanitizer (memcheck / racecheck /
-synccheck): every engine, both dtypes, colocated ranks, gather residual."""
+synccheck): every engine, both dtypes, colocated ranks (W 2/4/8), gather residual."""
 import os
 import sys
 
@@ -18,8 +18,10 @@ for H in (8192, 6144, 4096, 33):
         tw.rmsnorm_residual(x, r, w, residual_out=r)
         # two CTAs: each walks ~18 rows, wrapping the smem ring (both row groups)
         tw.rmsnorm_residual(x, r, w, sm_budget=2)
-for W in (2, 4):
-    T, H = 29, 1024
+# K1 PEER bulk-copy engine: one stage per row (W 2/4), two stages per row with
+# a lazily released (H 1024) and an immediately released (H 8192) ring
+for W, H in ((2, 1024), (4, 1024), (8, 1024), (8, 8192), (2, 8192)):
+    T = 29
     comm = tw.Communicator(W, [0] * W, T * H * 4, tw.TW_TRANSPORT_PEER)
     for dt in (torch.bfloat16, torch.float32):
         for q in range(W):
