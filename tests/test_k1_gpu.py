@@ -100,13 +100,16 @@ def test_k1_matches_golden_fixtures(cuda, golden):
         assert np.array_equal(np.concatenate(res), arrays[f"fused_{case['id']}_res"])
 
 
+@pytest.mark.parametrize("W,H", [(4, 256), (8, 1024), (8, 8192)])
 @pytest.mark.parametrize("dtype_name", ["float32", "bfloat16"])
-def test_k1_gather_residual(cuda, orc, dtype_name):
-    """G=2 (north_star): r' is all-gathered to every rank's RESIDUAL buffer."""
+def test_k1_gather_residual(cuda, orc, dtype_name, W, H):
+    """G=2 (north_star): r' is all-gathered to every rank's RESIDUAL buffer
+    (W = 8: the bulk-copy engine's two-stage rows, lazily and immediately
+    released rings)."""
     import torch
     import paper_2505_11329_b200 as tw
     dtype = getattr(torch, dtype_name)
-    W, T, H = 4, 37, 256
+    T = 37
     inputs, residual, weight = group_inputs(9, W, T, H)
     ranges = tw.token_shard_map(T, W)
     inputs, residual, want_out, want_res = oracle_case(orc, inputs, residual, weight, ranges,
