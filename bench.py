@@ -360,9 +360,9 @@ def run_ours_single(args):
             sweep[str(t)] = {"us": round(us, 2), "hbm_gbs": round((4 * t * H * 2) / us / 1e3, 1)}
         line["tp1_sweep"] = sweep
         line["unfused_torch_add_rmsnorm_us"] = unfused_torch(T, H, flush)
-        # simulated ranks share this GPU: the whole GPU (2 CTAs/SM) split between them
-        line["k1_colocated_peer_us"] = {f"tp{n}_ctas{296 // n}": k1_colocated(T, H, n, 296 // n, flush)
-                                        for n in (2, 8)}
+        # simulated ranks share this GPU: the whole GPU split between them (the
+        # library clamps the budget to what its engine can co-schedule)
+        line["k1_colocated_peer_us"] = {f"tp{n}": k1_colocated(T, H, n, 296 // n, flush) for n in (2, 4, 8)}
         # the weave: one Llama-3.3-70B layer at TP = 8 per-GPU
         # GEMM shapes, T = 8192, boundary op K2 (the one-GPU stand-in for K1)
         try:
