@@ -409,7 +409,9 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
       static const char* groups_env = std::getenv("TW_K2_GROUPS");
       q.groups = (sm_budget > 0 || T < 48LL * nsm || row_bytes < 16 * 1024) ? 2 : 1;
       if (groups_env) q.groups = std::max(1, std::min(2, std::atoi(groups_env)));
-      if (q.groups * bp.tpr > kBulkMaxConsumers) q.groups = 1;
+      // a group frees its stage one row late, so the ring needs more stages
+      // than groups (40 KB rows leave two stages: one group)
+      if (q.groups * bp.tpr > kBulkMaxConsumers || stages <= q.groups) q.groups = 1;
       q.stages = stages;
       q.row_bytes = row_bytes;
       q.eps = eps;

@@ -106,7 +106,7 @@ def test_k2_every_engine_matches_oracle(cuda, engine, pipeline, groups):
     env = dict(os.environ, TW_K2_ENGINE=engine, TW_ROWS_PIPELINE=pipeline, TW_K2_GROUPS=groups)
     p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
                         "matches_oracle and not every_engine or in_place or full_size or host_buffers "
-                        "or sm_budget"],
+                        "or sm_budget or under_budget"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-2000:]
     assert " passed" in p.stdout
@@ -174,6 +174,27 @@ def test_k2_sm_budget_does_not_change_results(cuda):
         o, rr = tw.rmsnorm_residual(x, r, w, sm_budget=budget)
         assert torch.equal(rr, ref_res)
         assert (o.float() - ref_out.float()).abs().max().item() <= 2 ** -7 * ref_out.float().abs().max().item()
+
+
+@pytest.mark.parametrize("H,dtype_name", [(10240, "float32"), (20480, "bfloat16")])
+def test_k2_two_stage_ring_under_budget(cuda, orc, H, dtype_name):
+    """40 KB rows leave room for a two-stage ring only: with a small SM budget
+    each CTA walks many rows, and the row-group count must stay below the ring
+    depth (a group frees its stage one row late)."""
+    import torch
+    T = 96
+    inp, res, w = norm_inputs(5 + H, T, H)
+    want_out, want_res = orc.rmsnorm_residual(bf16_round(inp), bf16_round(res), w) \
+        if dtype_name == "bfloat16" else orc.rmsnorm_residual(inp, res, w)
+    for budget in (2, 4):
+        if dtype_name == "bfloat16":
+            out, rout = run_k2(bf16_round(inp), bf16_round(res), w, torch.bfloat16, sm_budget=budget)
+            assert np.array_equal(rout, bf16_round(want_res))
+            assert_bf16_close(out, want_out)
+        else:
+            out, rout = run_k2(inp, res, w, torch.float32, sm_budget=budget)
+            assert np.array_equal(rout, want_res)
+            assert_abs_close(out, want_out, 1e-5)
 
 
 def test_k2_full_size_vs_torch_fp32_and_sampled_oracle(cuda, orc):

@@ -39,7 +39,11 @@ def child(tag):
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1:
+    if len(sys.argv) > 1 and sys.argv[1] == "--groups":  # TMA engine, 1 / 2 row groups
+        for g in ("1", "2"):
+            env = dict(os.environ, TW_K2_ENGINE="tma", TW_K2_CTAS_PER_SM="1", TW_K2_GROUPS=g)
+            subprocess.run([sys.executable, __file__, f"tma-cps1-g{g}"], env=env, check=True)
+    elif len(sys.argv) > 1:
         child(sys.argv[1])
     else:
         for eng, cps, g in (("tma", "1", "1"), ("tma", "2", "1"), ("tma", "1", "2"), ("bulk", "1", "1"),
