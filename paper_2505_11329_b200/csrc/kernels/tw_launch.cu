@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "tw_bulk.cuh"
 #include "tw_flat.cuh"
@@ -277,7 +278,9 @@ PeerTmaFn pick_peer_tma(int world, int vpt) {
 bool peer_tma_geometry(int world, long long H, bool bf16, int* stages, size_t* smem) {
   const size_t row = static_cast<size_t>(H) * (bf16 ? 2 : 4);
   const size_t stage = peer_tma_stage_rows(world) * row;
-  const int S = static_cast<int>(std::min<size_t>(4, (200 * 1024) / stage));
+  static const char* env = std::getenv("TW_K1_PEER_STAGES");  // A/B: ring depth cap
+  const int cap = env ? std::max(2, std::atoi(env)) : 4;
+  const int S = static_cast<int>(std::min<size_t>(cap, (200 * 1024) / stage));
   if (S < 2) return false;
   *stages = S;
   *smem = S * stage + 2 * S * sizeof(uint64_t) + 2 * 8 * sizeof(double);
