@@ -46,10 +46,21 @@ def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+def _current_raw_stream(device=None) -> int:
+    """The current CUDA stream handle of `device` (default: the current one);
+    torch's raw accessor costs ~0.3 us where torch.cuda.current_stream() costs
+    ~3 us per call, which is most of an op's host time at decode sizes
+    (tools/host_overhead.py)."""
+    import torch
+    torch.cuda._lazy_init()  # a flag check once initialised
+    if device is None:
+        device = torch._C._cuda_getDevice()
+    return torch._C._cuda_getCurrentRawStream(device)
+
+
 def _stream_handle(stream) -> int | None:
     if stream is None:
-        import torch
-        return torch.cuda.current_stream().cuda_stream
+        return _current_raw_stream()
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
@@ -187,7 +198,7 @@ class Communicator:
         if streams is not None:
             strs = (c_void_p * W)(*[_stream_handle(s) for s in streams])
         else:
-            strs = (c_void_p * W)(*[torch.cuda.current_stream(d).cuda_stream for d in self.devices])
+            strs = (c_void_p * W)(*[_current_raw_stream(d) for d in self.devices])
         check(_lib.lib.tw_fused_allreduce_rmsnorm_group(self._h, T, H, token_offset, ranges, res, wts, float(eps), code,
                                                         int(sm_budget), TW_GATHER_RESIDUAL if gather_residual else 0,
                                                         strs))
@@ -200,7 +211,7 @@ class Communicator:
         if streams is not None:
             strs = (c_void_p * W)(*[_stream_handle(s) for s in streams])
         else:
-            strs = (c_void_p * W)(*[torch.cuda.current_stream(d).cuda_stream for d in self.devices])
+            strs = (c_void_p * W)(*[_current_raw_stream(d) for d in self.devices])
         check(_lib.lib.tw_allreduce_group(self._h, T, H, token_offset, code, int(sm_budget), strs))
 
     def check(self) -> None:

@@ -715,7 +715,8 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
   p.H = H;
   p.row_offset = token_offset;
   p.eps = eps;
-  p.flags = flags;
+  // co-located ranks share one GPU: device-scope barrier fences suffice
+  p.flags = (flags & ~kDeviceScope) | (comm->colocated ? kDeviceScope : 0u);
   p.world = W;
   // Barrier poll bound (~2 s at the default) and the fault-injection hook of
   // the timeout path: TW_FAULT_DROP_ARRIVAL_RANK=r makes rank r never signal,

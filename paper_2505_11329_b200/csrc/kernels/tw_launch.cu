@@ -5,6 +5,9 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "tw_bulk.cuh"
 #include "tw_flat.cuh"
@@ -12,6 +15,49 @@
 #include "tw_rownorm.cuh"
 
 namespace tw {
+
+// ---- per-function launch setup, cached ---------------------------------------------
+// cudaFuncSetAttribute and the occupancy calculator cost microseconds of host
+// time per call; at decode sizes that is the whole op.  Both are per (function,
+// device) facts, so they are computed once (tools/host_overhead.py).
+namespace {
+std::mutex g_setup_mu;
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+}  // namespace
+
+cudaError_t ensure_dynamic_smem(const void* fn, size_t bytes) {
+  static std::map<std::pair<const void*, int>, size_t> set;
+  const auto key = std::make_pair(fn, current_device());
+  std::lock_guard<std::mutex> g(g_setup_mu);
+  auto it = set.find(key);
+  if (it != set.end() && it->second >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e == cudaSuccess) set[key] = bytes;
+  return e;
+}
+
+int cached_occupancy(const void* fn, int threads, size_t smem) {
+  static std::map<std::tuple<const void*, int, int, size_t>, int> occ;
+  const auto key = std::make_tuple(fn, current_device(), threads, smem);
+  {
+    std::lock_guard<std::mutex> g(g_setup_mu);
+    auto it = occ.find(key);
+    if (it != occ.end()) return it->second;
+  }
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  std::lock_guard<std::mutex> g(g_setup_mu);
+  occ[key] = n;
+  return n;
+}
 
 // ---- K3: one-shot AllReduce baseline (collectives.cpp:82-88 semantics) --------
 // Rank r reduces its token shard and broadcasts it: OUTPUT[t] = sum_q INPUT_q[t].
@@ -139,11 +185,7 @@ cudaError_t launch_allreduce(const RowParams& params, const RowPlan& plan, bool 
 int rownorm_blocks_per_sm(const RowPlan& plan, bool bf16, Xport x) {
   KernelFn fn = pick_kernel(bf16, plan.N, x, plan.vpt, plan.pipeline);
   if (!fn) return 0;
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reinterpret_cast<const void*>(fn), plan.groups * plan.tpr,
-                                                    0) != cudaSuccess)
-    return 0;
-  return n;
+  return cached_occupancy(reinterpret_cast<const void*>(fn), plan.groups * plan.tpr, 0);
 }
 
 // ---- K2 bulk-copy pipeline -------------------------------------------------------
@@ -180,8 +222,7 @@ cudaError_t launch_k2_bulk(const BulkParams& params, int vpt, bool bf16, int gri
   BulkFn fn = bf16 ? pick_bulk_e<uint16_t>(vpt, tma_store, p.groups) : pick_bulk_e<float>(vpt, tma_store, p.groups);
   if (!fn) return cudaErrorInvalidConfiguration;
   const size_t smem = bulk_smem_bytes(p.stages, p.row_bytes, p.tpr, p.groups);
-  cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(fn), smem);
   if (e != cudaSuccess) return e;
   void* args[] = {&p};
   return cudaLaunchKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(p.groups * p.tpr + 32), args, smem,
@@ -205,8 +246,7 @@ cudaError_t launch_k2_flat(const FlatParams& params, bool bf16, int sms, bool on
     return cudaErrorInvalidConfiguration;
   }
   const int threads = std::max(32, ((params.V + vpt - 1) / vpt + 31) / 32 * 32);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(fn), threads, 0);
+  int per_sm = one_cta_per_sm ? 1 : cached_occupancy(reinterpret_cast<const void*>(fn), threads, 0);
   if (one_cta_per_sm) per_sm = 1;  // an explicit SM budget: more CTAs would spread over more SMs
   const long long grid = std::min<long long>(params.T, static_cast<long long>(sms) * std::max(per_sm, 1));
   FlatParams p = params;
@@ -294,13 +334,8 @@ int k1_peer_tma_blocks_per_sm(int world, int V, long long H, bool bf16) {
   int S = 0;
   size_t smem = 0;
   if (!fn || !peer_tma_geometry(world, H, bf16, &S, &smem)) return 0;
-  if (cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem)) != cudaSuccess)
-    return 0;
-  int b = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, reinterpret_cast<const void*>(fn), 288, smem) != cudaSuccess)
-    return 0;
-  return b;
+  if (ensure_dynamic_smem(reinterpret_cast<const void*>(fn), smem) != cudaSuccess) return 0;
+  return cached_occupancy(reinterpret_cast<const void*>(fn), 288, smem);
 }
 
 cudaError_t launch_k1_peer_tma(RowParams params, int world, int V, bool bf16, dim3 grid, cudaStream_t stream) {
@@ -309,8 +344,7 @@ cudaError_t launch_k1_peer_tma(RowParams params, int world, int V, bool bf16, di
   int S = 0;
   size_t smem = 0;
   if (!fn || !peer_tma_geometry(world, params.H, bf16, &S, &smem)) return cudaErrorNotSupported;
-  cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+  cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(fn), smem);
   if (e != cudaSuccess) return e;
   params.V = V;
   params.nslots_stages = S;

@@ -212,7 +212,10 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
     if (storer) {
       bulk_wait_all();  // every store performed before the exit barrier signals
       asm volatile("fence.proxy.async.global;" ::: "memory");
-      fence_acq_rel_sys();
+      if (p.flags & kDeviceScope)
+        fence_acq_rel_gpu();
+      else
+        fence_acq_rel_sys();
     }
   }
   rank_barrier<Xport::Peer>(p, s, 2);

@@ -84,6 +84,7 @@ struct RowParams {
 };
 
 constexpr unsigned kGatherResidual = 0x1u;
+constexpr unsigned kDeviceScope = 0x100u;  // internal: every rank on this GPU (device-scope barriers)
 
 // ---- typed vector access -------------------------------------------------------
 // N elements of E per "vector": 8 x bf16 or 4 x f32 (16 B), or 1 element.
@@ -224,12 +225,18 @@ __device__ __forceinline__ void rank_barrier(const RowParams& p, const RankSlot&
       if constexpr (X == Xport::Nvls) {
         mm_red_release_add(p.mc_pad + b, 1u);  // one op reaches every rank's pad
       } else {
-        fence_acq_rel_sys();
-        for (int q = 0; q < p.world; ++q) red_relaxed_add(p.peer_pad[q] + b, 1u);
+        if (p.flags & kDeviceScope) {
+          fence_acq_rel_gpu();
+          for (int q = 0; q < p.world; ++q) red_relaxed_add_gpu(p.peer_pad[q] + b, 1u);
+        } else {
+          fence_acq_rel_sys();
+          for (int q = 0; q < p.world; ++q) red_relaxed_add(p.peer_pad[q] + b, 1u);
+        }
       }
     }
     long long spins = 0;
-    while (static_cast<int>(ld_acquire(s.pad + b) - target) < 0) {
+    const bool dev_scope = X != Xport::Nvls && (p.flags & kDeviceScope);
+    while (static_cast<int>((dev_scope ? ld_acquire_gpu(s.pad + b) : ld_acquire(s.pad + b)) - target) < 0) {
       if (++spins > p.spin_limit) {  // bounded: a rank was never launched / died
         atomicExch(p.err, 1);
         break;
