@@ -11,11 +11,14 @@
 // residual, write r' over the residual slot and the normed output over slot 0
 // of the final stage, and the storer thread bulk-stores r' to the local
 // shard, the output to every rank's OUTPUT (and r' to every rank's RESIDUAL
-// with G = 2).  W <= 4 takes one stage per row; W = 8 splits a row over two
-// stages (4 + 5 rows) so the ring still double-buffers inside the shared-
-// memory budget.  W and the chunking are compile-time, so every per-stage
-// sum is unrolled and its shared-memory loads issue together.  The rank
-// barriers are the row engine's (tw_rownorm.cuh).
+// with G = 2).  W <= 3 takes one stage per row; W = 4 and W = 8 split a row
+// over two stages (2 + 3 and 4 + 5 rows): smaller stages keep the ring 4 and
+// 2 deep inside the shared-memory budget (co-located, T = H = 8192: W = 4
+// 237 vs 257 us with one stage per row; W = 2 with two stages 184 vs 132 us,
+// W = 8 with three 384 vs 377 us -- profiles/k2_engines_r01.txt).  W and the
+// chunking are compile-time, so every per-stage sum is unrolled and its
+// shared-memory loads issue together.  The rank barriers are the row engine's
+// (tw_rownorm.cuh).
 #pragma once
 
 #include "tw_bulk.cuh"
@@ -24,7 +27,7 @@
 namespace tw {
 
 constexpr int kPeerTmaMaxWorld = kMaxRanks;
-__host__ __device__ constexpr int peer_tma_chunks(int W) { return W <= 4 ? 1 : 2; }
+__host__ __device__ constexpr int peer_tma_chunks(int W) { return W <= 3 ? 1 : 2; }
 __host__ __device__ constexpr int peer_tma_stage_rows(int W) {
   return (W + 1 + peer_tma_chunks(W) - 1) / peer_tma_chunks(W);
 }
