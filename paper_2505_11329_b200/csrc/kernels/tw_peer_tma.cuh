@@ -15,7 +15,8 @@
 // over two stages (2 + 3 and 4 + 5 rows): smaller stages keep the ring 4 and
 // 2 deep inside the shared-memory budget (co-located, T = H = 8192: W = 4
 // 237 vs 257 us with one stage per row; W = 2 with two stages 184 vs 132 us,
-// W = 8 with three 384 vs 377 us -- profiles/k2_engines_r01.txt).  W and the
+// W = 3 with two 209 vs 181 us, W = 8 with three 384 vs 377 us --
+// profiles/k2_engines_r01.txt).  W and the
 // chunking are compile-time, so every per-stage sum is unrolled and its
 // shared-memory loads issue together.  The rank barriers are the row engine's
 // (tw_rownorm.cuh).
