@@ -36,6 +36,10 @@ $(OBJDIR)/tw_launch.o: $(KSRC) $(KHDR)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
+$(OBJDIR)/tw_nvls.o: $(PKG)/csrc/kernels/tw_nvls.cu $(KHDR)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
 $(OBJDIR)/tw_capi.o: $(HSRC) $(HHDR) $(KHDR)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
@@ -48,7 +52,7 @@ $(OBJDIR)/tw_host_io.o: $(PKG)/csrc/host/tw_host_io.cu $(HHDR) $(KHDR)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
-$(LIBDIR)/libtw.so: $(OBJDIR)/tw_launch.o $(OBJDIR)/tw_capi.o $(OBJDIR)/tw_mp.o $(OBJDIR)/tw_host_io.o
+$(LIBDIR)/libtw.so: $(OBJDIR)/tw_launch.o $(OBJDIR)/tw_nvls.o $(OBJDIR)/tw_capi.o $(OBJDIR)/tw_mp.o $(OBJDIR)/tw_host_io.o
 	@mkdir -p $(LIBDIR)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $^ -Xlinker --exclude-libs,ALL
 

@@ -56,8 +56,18 @@ typedef enum tw_dtype { TW_BF16 = 0, TW_F32 = 1 } tw_dtype;
  *         between GPUs, or plain HBM when several simulated ranks share one
  *         device -- the reference's in-process RankGroup, collectives.hpp:34).
  *  AUTO : NVLS when every rank is on a distinct multicast-capable device,
- *         PEER otherwise. */
-typedef enum tw_transport { TW_TRANSPORT_AUTO = 0, TW_TRANSPORT_NVLS = 1, TW_TRANSPORT_PEER = 2 } tw_transport;
+ *         PEER otherwise.
+ *  NVLS_SIM : TEST transport for one GPU.  Simulated ranks sharing a device
+ *         run the NVLS kernels themselves (same instantiated control flow:
+ *         pipeline, barriers, generations, G = 2) with each multimem
+ *         instruction spelled as per-rank loads/stores/reductions.  Never
+ *         chosen by AUTO; co-located communicators only. */
+typedef enum tw_transport {
+  TW_TRANSPORT_AUTO = 0,
+  TW_TRANSPORT_NVLS = 1,
+  TW_TRANSPORT_PEER = 2,
+  TW_TRANSPORT_NVLS_SIM = 3
+} tw_transport;
 
 /* Symmetric buffers owned by a communicator (one per rank, same size). */
 typedef enum tw_buffer {
@@ -68,6 +78,9 @@ typedef enum tw_buffer {
 
 /* Flags for the fused op. */
 #define TW_GATHER_RESIDUAL 0x1u /* G=2: all-gather r' as well as the output  */
+/* NVLS kernel: rows of multimem.ld_reduce kept in flight per row group ahead
+ * of the row being normalised, d in 1..3 (0 / unset = 2). */
+#define TW_NVLS_DEPTH(d) ((((unsigned)(d)) & 0x3u) << 4)
 
 typedef struct tw_comm* tw_comm_t;
 
@@ -154,8 +167,8 @@ TW_API tw_status tw_fused_allreduce_rmsnorm_group(tw_comm_t comm, int64_t T, int
  * creates the NVLS multicast object and shares it by POSIX fd over an
  * abstract Unix socket.  Collective per-rank calls must be made in the same
  * order with the same shapes on every rank (the signal-pad epochs are
- * host-tracked).  transport: NVLS, PEER (cudaIpc-mapped peer buffers, NVLink
- * P2P), or AUTO = NVLS with a collective fallback to PEER. */
+ * device-resident, per CTA index).  transport: NVLS, PEER (cudaIpc-mapped peer
+ * buffers, NVLink P2P), or AUTO = NVLS with a collective fallback to PEER. */
 TW_API tw_status tw_comm_create_mp(int world, int rank, int device, size_t buffer_bytes, const char* rendezvous_id,
                                    tw_transport transport, tw_comm_t* out);
 /* K1 for the rank this process owns (multi-process communicators). */

@@ -13,7 +13,8 @@ from ctypes import c_int, c_int64, c_size_t, c_void_p
 
 from . import _lib
 from ._lib import (TW_BF16, TW_F32, TW_BUF_INPUT, TW_BUF_OUTPUT, TW_BUF_RESIDUAL, TW_GATHER_RESIDUAL,
-                   TW_TRANSPORT_AUTO, TW_TRANSPORT_NVLS, TW_TRANSPORT_PEER, BarrierTimeout, ConfigError,
+                   TW_TRANSPORT_AUTO, TW_TRANSPORT_NVLS, TW_TRANSPORT_NVLS_SIM, TW_TRANSPORT_PEER, TW_NVLS_DEPTH,
+                   BarrierTimeout, ConfigError,
                    ContractError, CudaError, DimensionError, NumericError, TwError, Unsupported, check,
                    shard_map_validate, token_shard_map)
 
@@ -21,6 +22,7 @@ __all__ = [
     "rmsnorm_residual", "Communicator", "token_shard_map", "shard_map_validate", "TwError", "DimensionError",
     "NumericError", "ConfigError", "ContractError", "CudaError", "BarrierTimeout", "Unsupported", "TW_BF16",
     "TW_F32", "TW_GATHER_RESIDUAL", "TW_TRANSPORT_AUTO", "TW_TRANSPORT_NVLS", "TW_TRANSPORT_PEER",
+    "TW_TRANSPORT_NVLS_SIM", "TW_NVLS_DEPTH",
     "device_count", "version",
 ]
 
@@ -181,8 +183,10 @@ class Communicator:
 
     def fused_allreduce_rmsnorm(self, T: int, H: int, residual_shards, weights, eps: float = 1e-5, *, dtype=None,
                                 shard_ranges=None, sm_budget: int = 8, gather_residual: bool = False, streams=None,
-                                token_offset: int = 0):
-        """Kernel K1 on every rank of this communicator (see tw.h)."""
+                                token_offset: int = 0, nvls_depth: int = 0):
+        """Kernel K1 on every rank of this communicator (see tw.h).  nvls_depth:
+        rows of ld_reduce in flight per row group on the NVLS kernel (1..3, 0 =
+        the library default)."""
         import torch
         W = self.world
         if dtype is None:
@@ -200,8 +204,9 @@ class Communicator:
         else:
             strs = (c_void_p * W)(*[_current_raw_stream(d) for d in self.devices])
         check(_lib.lib.tw_fused_allreduce_rmsnorm_group(self._h, T, H, token_offset, ranges, res, wts, float(eps), code,
-                                                        int(sm_budget), TW_GATHER_RESIDUAL if gather_residual else 0,
-                                                        strs))
+                                                        int(sm_budget),
+                                                        (TW_GATHER_RESIDUAL if gather_residual else 0)
+                                                        | TW_NVLS_DEPTH(nvls_depth), strs))
 
     def allreduce(self, T: int, H: int, dtype, *, sm_budget: int = 8, streams=None, token_offset: int = 0):
         """Unfused AllReduce baseline (K3): OUTPUT = sum_r INPUT on every rank."""

@@ -16,10 +16,16 @@ LIB_PATH = os.path.join(_HERE, "lib", "libtw.so")
 TW_OK, TW_ERR_DIMENSION, TW_ERR_NUMERIC, TW_ERR_CONFIG, TW_ERR_CONTRACT, TW_ERR_CUDA, TW_ERR_TIMEOUT, \
     TW_ERR_UNSUPPORTED, TW_ERR_PARSE = range(9)
 TW_BF16, TW_F32 = 0, 1
-TW_TRANSPORT_AUTO, TW_TRANSPORT_NVLS, TW_TRANSPORT_PEER = 0, 1, 2
+TW_TRANSPORT_AUTO, TW_TRANSPORT_NVLS, TW_TRANSPORT_PEER, TW_TRANSPORT_NVLS_SIM = 0, 1, 2, 3
 TW_BUF_INPUT, TW_BUF_OUTPUT, TW_BUF_RESIDUAL = 0, 1, 2
 TW_GATHER_RESIDUAL = 0x1
-TRANSPORT_NAMES = {TW_TRANSPORT_AUTO: "auto", TW_TRANSPORT_NVLS: "nvls", TW_TRANSPORT_PEER: "peer"}
+TRANSPORT_NAMES = {TW_TRANSPORT_AUTO: "auto", TW_TRANSPORT_NVLS: "nvls", TW_TRANSPORT_PEER: "peer",
+                   TW_TRANSPORT_NVLS_SIM: "nvls_sim"}
+
+
+def TW_NVLS_DEPTH(d: int) -> int:
+    """Flag bits of the NVLS kernel's pipeline depth (tw.h TW_NVLS_DEPTH)."""
+    return (int(d) & 0x3) << 4
 
 
 class TwError(RuntimeError):

@@ -383,10 +383,12 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
     // keeps the older two-CTA half-ring mode for A/B.
     int cps = 1;
     if (cps_env) cps = std::max(1, std::min(4, std::atoi(cps_env)));
-    int stages = static_cast<int>(std::min<size_t>(8, (200 * 1024 / cps) / (2ull * row_bytes)));
+    static const char* ring_env = std::getenv("TW_K2_RING_KB");  // A/B: shared-memory ring budget
+    const size_t ring = static_cast<size_t>(ring_env ? std::max(64, std::min(224, std::atoi(ring_env))) : 200) * 1024;
+    int stages = static_cast<int>(std::min<size_t>(8, (ring / cps) / (2ull * row_bytes)));
     if (stages < 2 && cps > 1) {  // long rows (>= 25 KB): one CTA per SM keeps a 2+ stage ring
       cps = 1;
-      stages = static_cast<int>(std::min<size_t>(8, (200 * 1024) / (2ull * row_bytes)));
+      stages = static_cast<int>(std::min<size_t>(8, ring / (2ull * row_bytes)));
     }
     if (plan_rows(H, nv, H / nv > 1024 ? 512 : 256, &bp) && bp.vpt <= 8 && bp.tpr <= kBulkMaxConsumers &&
         stages >= 2) {
@@ -462,6 +464,8 @@ tw_status tw_comm_create(int world, const int* devices, size_t buffer_bytes, tw_
   if (world < 1 || world > kMaxRanks)
     return fail(TW_ERR_CONFIG, "comm_create: world must be in [1, " + std::to_string(kMaxRanks) + "]");
   if (!devices) return fail(TW_ERR_CONFIG, "comm_create: null device list");
+  if (transport < TW_TRANSPORT_AUTO || transport > TW_TRANSPORT_NVLS_SIM)
+    return fail(TW_ERR_CONFIG, "comm_create: unknown transport");
   const int ndev = tw_device_count();
   if (ndev == 0) return fail(TW_ERR_CUDA, "comm_create: no CUDA device visible");
   DeviceGuard guard;
@@ -486,7 +490,15 @@ tw_status tw_comm_create(int world, const int* devices, size_t buffer_bytes, tw_
     return fail(TW_ERR_CONFIG, "comm_create: ranks must be all on one device or all on distinct devices");
   }
   tw_status st;
-  if (transport == TW_TRANSPORT_NVLS || (transport == TW_TRANSPORT_AUTO && distinct && world >= 2)) {
+  if (transport == TW_TRANSPORT_NVLS_SIM) {
+    // test transport: the NVLS kernels on simulated ranks sharing one device
+    if (!c->colocated || world < 2) {
+      delete c;
+      return fail(TW_ERR_UNSUPPORTED, "NVLS_SIM transport needs >= 2 simulated ranks on one device");
+    }
+    c->transport = TW_TRANSPORT_NVLS_SIM;
+    st = create_peer(c);
+  } else if (transport == TW_TRANSPORT_NVLS || (transport == TW_TRANSPORT_AUTO && distinct && world >= 2)) {
     c->transport = TW_TRANSPORT_NVLS;
     if (!distinct || world < 2) {
       delete c;
@@ -664,7 +676,8 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
     }
   }
   if (T == 0) return TW_OK;
-  const bool nvls = comm->transport == TW_TRANSPORT_NVLS;
+  const bool sim = comm->transport == TW_TRANSPORT_NVLS_SIM;
+  const bool nvls = comm->transport == TW_TRANSPORT_NVLS || sim;  // the NVLS kernels (tw_nvls.cuh)
   const int nv = bf16 ? 8 : 4;
   bool vec = H % nv == 0;
   if (fused) {
@@ -677,13 +690,17 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
     return fail(TW_ERR_UNSUPPORTED, std::string(op) + ": NVLS transport needs H % " + std::to_string(nv) +
                                         " == 0 and 16-byte aligned buffers");
   RowPlan plan;
-  // NVLS: 256-thread row groups, <= 4 vectors per thread so the software
-  // pipeline (next row's ld_reduce in flight) fits two register sets; PEER
-  // holds every rank's vector before summing, so it uses wider groups.
+  // NVLS: 256-thread row groups (two per CTA), <= 4 vectors per thread so the
+  // D + 1 in-flight register sets of the pipeline stay spill-free; PEER holds
+  // every rank's vector before summing, so it uses wider groups.
   const long long nvec = H / (vec ? nv : 1);
   if (!plan_rows(H, vec ? nv : 1, nvls ? (nvec > 1024 ? 512 : 256) : 512, &plan))
     return fail(TW_ERR_DIMENSION, std::string(op) + ": hidden size too large for the row engine");
+  if (nvls && !nvls_supported(plan))
+    return fail(TW_ERR_UNSUPPORTED, std::string(op) + ": NVLS kernel supports H <= " + std::to_string(bf16 ? 16384 : 8192) +
+                                        " for this dtype");
   const Xport x = nvls ? Xport::Nvls : Xport::Peer;
+  const int depth = nvls_depth_from_flags(flags);
 
   DeviceGuard guard;
   int budget = sm_budget > 0 ? sm_budget : 8;
@@ -698,7 +715,12 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
   int peer_tma_bpsm = 0;
   if (fused && !nvls && vec && W <= kPeerTmaMaxWorld && !(peer_env && std::strcmp(peer_env, "rows") == 0))
     peer_tma_bpsm = k1_peer_tma_blocks_per_sm(W, static_cast<int>(H / nv), H, bf16);
-  if (peer_tma_bpsm > 0) {
+  if (nvls) {
+    // every CTA of every co-launched rank resident for the barrier (the
+    // hardware path has one rank per GPU: the budget is simply SMs)
+    const int bpsm = fused ? std::max(1, k1_nvls_blocks_per_sm(plan, bf16, sim, depth)) : 1;
+    budget = std::min(budget, std::max(1, sms * bpsm / (comm->colocated ? W : 1)));
+  } else if (peer_tma_bpsm > 0) {
     const int slots = comm->colocated ? W : 1;
     budget = std::min(budget, std::max(1, sms * peer_tma_bpsm / slots));
   } else if (fused) {
@@ -716,7 +738,7 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
   p.row_offset = token_offset;
   p.eps = eps;
   // co-located ranks share one GPU: device-scope barrier fences suffice
-  p.flags = (flags & ~kDeviceScope) | (comm->colocated ? kDeviceScope : 0u);
+  p.flags = (flags & ~(kDeviceScope | kNvlsDepthMask)) | (comm->colocated ? kDeviceScope : 0u);
   p.world = W;
   // Barrier poll bound (~2 s at the default) and the fault-injection hook of
   // the timeout path: TW_FAULT_DROP_ARRIVAL_RANK=r makes rank r never signal,
@@ -743,6 +765,8 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
     s.gen = comm->ranks[r].gen;
   };
   auto launch = [&](const RowParams& pp, dim3 grid, cudaStream_t s) {
+    if (nvls)
+      return fused ? launch_k1_nvls(pp, plan, bf16, sim, depth, grid, s) : launch_k3_nvls(pp, plan, bf16, sim, grid, s);
     if (peer_tma_bpsm > 0) return launch_k1_peer_tma(pp, W, static_cast<int>(H / nv), bf16, grid, s);
     return fused ? launch_rownorm(pp, plan, bf16, x, grid, s) : launch_allreduce(pp, plan, bf16, x, grid, s);
   };

@@ -375,6 +375,8 @@ tw_status tw_comm_create_mp(int world, int rank, int device, size_t buffer_bytes
   if (world < 2 || world > 8) return fail(TW_ERR_CONFIG, "comm_create_mp: world must be in [2, 8]");
   if (rank < 0 || rank >= world) return fail(TW_ERR_CONFIG, "comm_create_mp: rank out of range");
   if (!rendezvous_id || !*rendezvous_id) return fail(TW_ERR_CONFIG, "comm_create_mp: empty rendezvous id");
+  if (transport != TW_TRANSPORT_AUTO && transport != TW_TRANSPORT_NVLS && transport != TW_TRANSPORT_PEER)
+    return fail(TW_ERR_CONFIG, "comm_create_mp: transport must be AUTO, NVLS or PEER");
   const int ndev = tw_device_count();
   if (ndev == 0) return fail(TW_ERR_CUDA, "comm_create_mp: no CUDA device visible");
   if (device < 0 || device >= ndev) return fail(TW_ERR_CONFIG, "comm_create_mp: device out of range");

@@ -114,9 +114,7 @@ KernelFn pick_by_xport(Xport x, int vpt, bool pipeline) {
     case Xport::Local:
       return pipeline ? pick_rownorm<E, N, Xport::Local, true>(vpt) : pick_rownorm<E, N, Xport::Local, false>(vpt);
     case Xport::Peer: return pick_rownorm<E, N, Xport::Peer, false>(vpt);
-    case Xport::Nvls:
-      if constexpr (N > 1) return pick_rownorm<E, N, Xport::Nvls, true>(vpt);
-      return nullptr;
+    case Xport::Nvls: return nullptr;  // k1_nvls_kernel (tw_nvls.cuh)
   }
   return nullptr;
 }
@@ -128,11 +126,7 @@ KernelFn pick_kernel(bool bf16, int N, Xport x, int vpt, bool pipeline) {
 }
 
 KernelFn pick_allreduce(bool bf16, int N, Xport x) {
-  if (x == Xport::Nvls) {
-    if (bf16 && N == 8) return allreduce_kernel<uint16_t, 8, Xport::Nvls>;
-    if (!bf16 && N == 4) return allreduce_kernel<float, 4, Xport::Nvls>;
-    return nullptr;
-  }
+  if (x == Xport::Nvls) return nullptr;  // k3_nvls_kernel (tw_nvls.cuh)
   if (bf16) return N == 8 ? allreduce_kernel<uint16_t, 8, Xport::Peer> : allreduce_kernel<uint16_t, 1, Xport::Peer>;
   return N == 4 ? allreduce_kernel<float, 4, Xport::Peer> : allreduce_kernel<float, 1, Xport::Peer>;
 }

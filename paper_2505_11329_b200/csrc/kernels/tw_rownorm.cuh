@@ -94,6 +94,7 @@ struct Vec;
 
 template <>
 struct Vec<uint16_t, 8> {  // bf16 x 8
+  static constexpr int kElems = 8;
   using Raw = uint4;
   static __device__ __forceinline__ Raw load(const void* base, long long e) {
     return ld_v4(static_cast<const uint16_t*>(base) + e);
@@ -122,6 +123,7 @@ struct Vec<uint16_t, 8> {  // bf16 x 8
 
 template <>
 struct Vec<float, 4> {  // f32 x 4
+  static constexpr int kElems = 4;
   using Raw = uint4;
   static __device__ __forceinline__ Raw load(const void* base, long long e) {
     return ld_v4(static_cast<const float*>(base) + e);
@@ -150,6 +152,7 @@ struct Vec<float, 4> {  // f32 x 4
 
 template <>
 struct Vec<uint16_t, 1> {  // scalar bf16 (H not a multiple of 8)
+  static constexpr int kElems = 1;
   using Raw = uint32_t;
   static __device__ __forceinline__ Raw load(const void* base, long long e) {
     return static_cast<const uint16_t*>(base)[e];
@@ -166,6 +169,7 @@ struct Vec<uint16_t, 1> {  // scalar bf16 (H not a multiple of 8)
 
 template <>
 struct Vec<float, 1> {  // scalar f32 (H not a multiple of 4)
+  static constexpr int kElems = 1;
   using Raw = uint32_t;
   static __device__ __forceinline__ Raw load(const void* base, long long e) {
     return __float_as_uint(static_cast<const float*>(base)[e]);

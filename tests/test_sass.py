@@ -48,16 +48,25 @@ def test_only_sm_100a_code():
 
 
 def test_nvls_fused_op_uses_multimem(sass):
+    """k1_nvls_kernel<E, VPT, D, MmHw>: in-switch reduction, multicast stores,
+    multicast release-add; the MmSim instantiations (one-GPU test transport)
+    of the same template contain none of them."""
     funcs = _functions(sass)
-    nvls = {k: v for k, v in funcs.items() if "rownorm_kernel" in k and "XportE2" in k}
-    assert nvls, "no NVLS rownorm instantiation"
-    for name, body in nvls.items():
+    hw = {k: v for k, v in funcs.items() if "k1_nvls_kernel" in k and "MmHw" in k}
+    sim = {k: v for k, v in funcs.items() if "k1_nvls_kernel" in k and "MmSim" in k}
+    assert len(hw) == 2 * 3 * 3 and len(sim) == len(hw), (sorted(hw), sorted(sim))  # {fp32,bf16} x VPT x depth
+    for name, body in hw.items():
         assert "LDGMC" in body, f"{name}: no multimem.ld_reduce (LDGMC)"     # RS in the switch
         assert "STG.E" in body and ".SYS" in body, name                      # multimem stores (system scope)
         assert "REDG" in body or "RED" in body, name                         # barrier signals
-    # the bf16 H=8192 instantiation (4 vectors per thread, pipelined) reduces in fp32 in the switch
-    bf16 = [b for k, b in nvls.items() if "rownorm_kernelItLi8ELi4ELNS_5XportE2ELb1E" in k]
+        assert "FENCE.VIEW.ASYNC" in body or "MEMBAR" in body or "FENCE" in body, name
+    for name, body in sim.items():
+        assert "LDGMC" not in body, name
+    # the bf16 H=8192 instantiation (4 vectors per thread) reduces in fp32 in the switch
+    bf16 = [b for k, b in hw.items() if "k1_nvls_kernelItLi4ELi2ENS_4MmHw" in k]
     assert bf16 and "HPADD.BF16" in bf16[0]
+    k3 = {k: v for k, v in funcs.items() if "k3_nvls_kernel" in k and "MmHw" in k}
+    assert len(k3) == 2 and all("LDGMC" in v for v in k3.values())
 
 
 def test_k2_tma_engine_uses_bulk_copies(sass):
@@ -83,7 +92,8 @@ def test_hot_kernels_do_not_spill():
     res = dict(re.findall(r"Function (\S+):\s*\n\s*(REG:.*)", usage))
     hot = ["_ZN2tw13k2_tma_kernelItLi4ELi1EEEvNS_10BulkParamsE",   # K2, bench shape (one row group)
            "_ZN2tw13k2_tma_kernelItLi4ELi2EEEvNS_10BulkParamsE",   # K2, two row groups
-           "_ZN2tw14rownorm_kernelItLi8ELi4ELNS_5XportE2ELb1EEEvNS_9RowParamsE",  # K1 NVLS, H=8192 bf16
+           "_ZN2tw14k1_nvls_kernelItLi4ELi2ENS_4MmHwEEEvNS_9RowParamsE",  # K1 NVLS, H=8192 bf16, depth 2
+           "_ZN2tw14k1_nvls_kernelItLi4ELi1ENS_4MmHwEEEvNS_9RowParamsE",  # depth 1
            "_ZN2tw18k1_peer_tma_kernelItLi4ELi2EEEvNS_9RowParamsE",   # K1 PEER bulk-copy, TP=2 H=8192 bf16
            "_ZN2tw18k1_peer_tma_kernelItLi4ELi8EEEvNS_9RowParamsE"]   # TP=8: two stages per row
     for k in hot:
