@@ -26,9 +26,9 @@ HHDR := $(PKG)/csrc/host/tw_internal.h include/tw/tw.h
 SHIM_SRC := $(wildcard $(PKG)/csrc/host/weavesim_*.cpp)
 SHIM_HDR := $(wildcard include/weavesim/*.hpp)
 
-.PHONY: all lib shim weave oracle ref cpptests clean
+.PHONY: all lib shim weave oracle ref cpptests benchtools clean
 
-all: lib shim weave oracle cpptests
+all: lib shim weave oracle cpptests benchtools
 
 lib: $(LIBDIR)/libtw.so
 
@@ -75,6 +75,13 @@ cpptests: build/tests/test_dropin
 
 build/tests/test_dropin: tests/cpp/test_dropin.cpp $(SHIM_HDR) $(LIBDIR)/libweavesim_b200.so
 	@mkdir -p build/tests
+	$(CXX) -std=c++20 -O2 -Iinclude -o $@ $< -L$(LIBDIR) -lweavesim_b200 -ltw -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' $(STDCXX)
+
+# The reference's C++ API timed through the drop-in (bench.py's e2e_dropin_f32).
+benchtools: build/bench/dropin_bench
+
+build/bench/dropin_bench: tools/dropin_bench.cpp $(SHIM_HDR) $(LIBDIR)/libweavesim_b200.so
+	@mkdir -p build/bench
 	$(CXX) -std=c++20 -O2 -Iinclude -o $@ $< -L$(LIBDIR) -lweavesim_b200 -ltw -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)' $(STDCXX)
 
 oracle:

@@ -13,11 +13,14 @@ better.  `e2e` is the same op through the C-ABI with pinned HOST buffers
 (H2D of input+residual and D2H of output+residual inside the timed region).
 
 N>1 (torchrun, one process per GPU): TP=N fused AllReduce + residual + RMSNorm
-(kernel K1) over the multi-process NVLS communicator (tools/bench_tp.py).
+(kernel K1) over the multi-process NVLS communicator at an 8-SM budget
+(tools/bench_tp.py; NVLS or fail -- no silent PEER fallback).  Without
+torchrun, `--gpus N` re-launches itself under torch.distributed.run.
 
 --impl reference: the reference's own CPU implementation of the path
-(oracle/_ref = proj/src/numerics.cpp compiled unmodified) on the host cores,
-same config / metric / unit.
+(oracle/_ref = proj/src/numerics.cpp / collectives.cpp compiled unmodified) on
+the host cores, same config / metric / unit: rmsnorm_residual at N=1,
+fused_allreduce_rmsnorm(parallel=true) with N ranks at N>1, full workload.
 """
 from __future__ import annotations
 
@@ -30,15 +33,11 @@ import sys
 import threading
 import time
 
-ROOT_DIR = os.path.dirname(os.path.abspath(__file__))
-if ROOT_DIR not in sys.path:
-    sys.path.insert(0, ROOT_DIR)
-# our libraries (and the CUDA toolkit's cuBLAS the weave runner is built
-# against) load before torch does -- see paper_2505_11329_b200/_lib.py
-import paper_2505_11329_b200  # noqa: E402,F401
-
 ROOT = os.path.dirname(os.path.abspath(__file__))
-sys.path.insert(0, ROOT)
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+# NOTE: the product package is imported only inside our arm (main(), after the
+# --impl dispatch), so the reference arm's process maps oracle/_ref alone.
 
 METRIC = "fused AR+RMSNorm µs & NVLink GB/s, 1024–8192 tok × 8192 hid, TP=1/2/4/8"
 UNIT = "us"
@@ -128,73 +127,68 @@ class ClockSampler:
 
 # ---- reference CPU arm ----------------------------------------------------------------
 
-def reference_rmsnorm_ms(T, H, threads, iters):
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def reference_rmsnorm_each_ms(T, H, threads, iters):
     """weavesim::rmsnorm_residual (oracle/_ref, the reference sources compiled
-    unmodified), token rows chunked over `threads` host threads."""
+    unmodified), token rows chunked over `threads` host threads; every
+    iteration's ms on one set of inputs (generated once, outside the clock)."""
     import oracle  # cpu_baseline / --impl reference legs only
-    return oracle.RefLib().time_rmsnorm(T, H, threads, iters)
+    return oracle.RefLib().time_rmsnorm(T, H, threads, iters, each=True)
+
+
+def _reference_line(args, world, us, ms, sample, cores, workload):
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(us / 1e3, 3), "higher_is_better": False,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic U(-1,1) fp32 inputs, unit weight (mt19937_64, the reference tests' draws)",
+        "config": {"workload": workload, "tokens": args.tokens, "hidden": args.hidden, "tp": world},
+        "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": cores, "kind": "reference",
+                         "cpu": cpu_model(), "host_threads_available": os.cpu_count(), "sample": sample},
+        "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_ms": [round(x, 2) for x in ms],
+        "gpu_launches": 0,
+    }
 
 
 def run_reference_arm(args):
+    """The reference's own CPU code (oracle/_ref), full workload every step:
+    N = 1 -> weavesim::rmsnorm_residual over all host threads (token chunks);
+    N > 1 -> weavesim::fused_allreduce_rmsnorm with N ranks, parallel=true
+    (proj/src/collectives.cpp:157-182: one std::thread per rank, validation
+    included).  Under torchrun only rank 0 runs."""
     if int(os.environ.get("RANK", "0")) != 0:
         return 0
     world = max(args.gpus, int(os.environ.get("WORLD_SIZE", "1")))
+    T, H = args.tokens, args.hidden
+    t0 = time.perf_counter()
     if world > 1:
-        return run_reference_arm_tp(args, world)
-    T, H = args.tokens, args.hidden
-    threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        reference_rmsnorm_ms(T, H, threads, 1)
-    t0 = time.perf_counter()
-    ms = [reference_rmsnorm_ms(T, H, threads, 1) for _ in range(args.steps)]
+        import oracle  # --impl reference leg only
+        ms = oracle.RefLib().time_fused(world, T, H, True, args.warmup + args.steps, each=True)[args.warmup:]
+        cores = world
+        sample = (f"full workload every step ({world} ranks x {T}x{H} fp32 partials + residual shards), "
+                  f"weavesim::fused_allreduce_rmsnorm(parallel=true): one std::thread per rank")
+        workload = (f"TP={world} fused AllReduce+residual+RMSNorm, {T} tok x {H} hid "
+                    f"(reference CPU path, {world} in-process ranks)")
+    else:
+        cores = os.cpu_count() or 1
+        ms = reference_rmsnorm_each_ms(T, H, cores, args.warmup + args.steps)[args.warmup:]
+        sample = (f"full workload every step ({T}x{H} fp32): token rows chunked over {cores} threads, "
+                  f"each calling weavesim::rmsnorm_residual")
+        workload = f"TP=1 fused residual-add+RMSNorm, {T} tok x {H} hid (reference CPU path)"
     wall = time.perf_counter() - t0
     us = 1e3 * sum(ms) / len(ms)
-    line = {
-        "impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(us / 1e3, 3), "higher_is_better": False,
-        "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic U(-1,1) inputs, unit weight",
-        "config": {"workload": f"TP=1 fused residual-add+RMSNorm, {T} tok x {H} hid (reference CPU path)",
-                   "tokens": T, "hidden": H, "tp": 1},
-        "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"full workload every step ({T}x{H} fp32): token rows chunked over {threads} "
-                                   f"threads, each calling weavesim::rmsnorm_residual; wall {wall:.1f}s"},
-        "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gpu_launches": 0,
-    }
-    print(json.dumps(line), flush=True)
-    return 0
-
-
-def run_reference_arm_tp(args, world):
-    """TP = N config: the reference's own fused_allreduce_rmsnorm
-    (proj/src/collectives.cpp:157-182) with N in-process ranks on N
-    std::threads (parallel=true, its fastest mode), including its validation.
-    Each step is a bounded row sample scaled to the full T."""
-    import oracle  # --impl reference leg only
-    ref = oracle.RefLib()
-    T, H = args.tokens, args.hidden
-    sample_T = min(T, 1024)
-    for _ in range(args.warmup):
-        ref.time_fused(world, sample_T, H, True, 1)
-    t0 = time.perf_counter()
-    ms = [ref.time_fused(world, sample_T, H, True, 1) * T / sample_T for _ in range(args.steps)]
-    wall = time.perf_counter() - t0
-    us = 1e3 * sum(ms) / len(ms)
-    line = {
-        "impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(us / 1e3, 3), "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic U(-1,1) inputs, unit weight",
-        "config": {"workload": f"TP={world} fused AllReduce+residual+RMSNorm, {T} tok x {H} hid "
-                               f"(reference CPU path, {world} simulated ranks)", "tokens": T, "hidden": H,
-                   "tp": world},
-        "cpu_baseline": {"value": round(us, 1), "unit": UNIT, "cores": world, "kind": "reference",
-                         "sample": f"{sample_T}-token sample per step ({world} ranks x {sample_T}x{H} fp32, "
-                                   f"parallel=true: one std::thread per rank), scaled x{T / sample_T:g}; "
-                                   f"wall {wall:.1f}s"},
-        "e2e": {"value": round(us, 1), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "gpu_launches": 0,
-    }
+    line = _reference_line(args, world, us, ms, sample + f"; wall {wall:.1f}s incl. input generation", cores,
+                           workload)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -315,6 +309,62 @@ def k1_colocated(T, H, world, budget, flush, reps=10):
     return round(1e3 * statistics.median(ts), 1)
 
 
+def k2_back_to_back(bufs, steps, stream_reps=1):
+    """Steady-state K2: `steps` launches back to back (no flush between them),
+    one event pair around the batch, so each launch also pays the previous
+    one's dirty-line write-back -- reported beside the flushed per-step mean."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    x, r, w, out, rout = bufs
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        for _ in range(3):
+            tw.rmsnorm_residual(x, r, w, EPS, residual_out=rout, out=out, stream=stream)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(steps):
+        tw.rmsnorm_residual(x, r, w, EPS, residual_out=rout, out=out, stream=stream)
+    e.record(stream)
+    torch.cuda.synchronize()
+    return 1e3 * s.elapsed_time(e) / steps
+
+
+def dropin_f32_e2e(T, H, steps):
+    """The reference's own C++ API and dtype through the drop-in:
+    weavesim::rmsnorm_residual(TokenMatrix fp32, ...) from
+    build/bench/dropin_bench (tools/dropin_bench.cpp, linked against
+    libweavesim_b200.so) -- host fp32 matrices in and out, the reference's
+    validation order, H2D | K2 | D2H inside; wall clock per call."""
+    exe = os.path.join(ROOT, "build", "bench", "dropin_bench")
+    if not os.path.exists(exe):
+        return {"error": f"{exe} not built (make benchtools)"}
+    try:
+        p = subprocess.run([exe, "rmsnorm", str(T), str(H), "2", str(steps)], capture_output=True, text=True,
+                           timeout=600)
+        d = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1])
+    except Exception as exc:  # noqa: BLE001 -- reported, not fatal
+        return {"error": str(exc)[:200]}
+    return {"value": round(1e3 * d["median_ms"], 1), "unit": UNIT, "dtype": "f32",
+            "h2d_bytes_per_step": d["h2d_bytes"], "d2h_bytes_per_step": d["d2h_bytes"], "steps": steps,
+            "stat": "median wall time per call", "mean": round(1e3 * d["mean_ms"], 1),
+            "min": round(1e3 * d["min_ms"], 1), "max": round(1e3 * d["max_ms"], 1),
+            "path": "weavesim::rmsnorm_residual (reference C++ API, proj/include/weavesim/numerics.hpp:42-43) "
+                    "linked against libweavesim_b200.so: fp32 TokenMatrix in/out, same config and dtype as "
+                    "--impl reference"}
+
+
+def k2_traffic():
+    """DRAM bytes per K2 launch from the newest committed ncu --set full capture."""
+    for name in ("k2_ncu_r02.json", "k2_ncu_r01.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                return json.load(f).get("dram_bytes_per_launch"), name
+        except Exception:
+            continue
+    return None, None
+
+
 def run_ours_single(args):
     import torch
     T, H = args.tokens, args.hidden
@@ -329,12 +379,7 @@ def run_ours_single(args):
     avg_us = 1e3 * sum(times_ms) / len(times_ms)
     alg_bytes = 4 * T * H * 2 + 4 * H  # read input+residual, write residual_out+output (bf16) + fp32 weight
     achieved = alg_bytes / (avg_us * 1e-6) / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "k2_ncu_r01.json")) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
-    except Exception:
-        pass
+    traffic, traffic_src = k2_traffic()
     line = {
         "metric": METRIC, "value": round(avg_us, 3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(avg_us / 1e3, 6), "higher_is_better": False,
@@ -345,24 +390,29 @@ def run_ours_single(args):
                    "tokens": T, "hidden": H, "tp": 1, "sm_budget": "whole GPU (148 SMs)", "l2": FLUSH_NOTE},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "peak_kind": peak_kind,
-                     "alg_bytes_per_launch": alg_bytes, "traffic": traffic},
+                     "alg_bytes_per_launch": alg_bytes, "traffic": traffic, "traffic_source": traffic_src},
         "e2e": e2e,
         "gpu_launches": args.steps,
-        "kernel_us": {"median": round(1e3 * statistics.median(times_ms), 3),
-                      "min": round(1e3 * min(times_ms), 3), "max": round(1e3 * max(times_ms), 3)},
+        "kernel_us": {"mean": round(avg_us, 3), "median": round(1e3 * statistics.median(times_ms), 3),
+                      "min": round(1e3 * min(times_ms), 3), "max": round(1e3 * max(times_ms), 3),
+                      "back_to_back_no_flush": round(k2_back_to_back(bufs, args.steps), 3)},
         "clocks": clk.summary(),
     }
     if not args.quick:
+        line["e2e_dropin_f32"] = dropin_f32_e2e(T, H, max(3, min(args.steps, 10)))
         sweep = {}
-        for t in (1024, 2048, 4096, 8192):
+        for t in (256, 1024, 2048, 4096, 8192, 16384):
             ts, _ = k2_timed(t, H, 20, 3, flush, seed=1)
             us = 1e3 * statistics.median(ts)
-            sweep[str(t)] = {"us": round(us, 2), "hbm_gbs": round((4 * t * H * 2) / us / 1e3, 1)}
+            sweep[str(t)] = {"us": round(us, 2), "hbm_gbs": round((4 * t * H * 2) / us / 1e3, 1),
+                             "frac": round((4 * t * H * 2) / us / 1e3 / peak, 3)}
         line["tp1_sweep"] = sweep
         line["unfused_torch_add_rmsnorm_us"] = unfused_torch(T, H, flush)
         # simulated ranks share this GPU: the whole GPU split between them (the
         # library clamps the budget to what its engine can co-schedule)
         line["k1_colocated_peer_us"] = {f"tp{n}": k1_colocated(T, H, n, 296 // n, flush) for n in (2, 4, 8)}
+        line["k1_colocated_note"] = ("N simulated ranks on this one GPU (PEER): HBM-bound data-movement stand-in, "
+                                     "not an NVLink number")
         # the weave: one Llama-3.3-70B layer at TP = 8 per-GPU
         # GEMM shapes, T = 8192, boundary op K2 (the one-GPU stand-in for K1)
         try:
@@ -370,26 +420,40 @@ def run_ours_single(args):
             r = weave.LayerRunner("llama-70b", tp=8, max_tokens=T)
             a, _, _, _ = weave.make_split_plan(T, threshold=r.threshold)
             line["weave_llama70b_tp8_shapes_us"] = {
-                "T": T, "unfused": round(r.run(T, "unfused", layers=6), 1),
+                "T": T, "prefix": a, "unfused": round(r.run(T, "unfused", layers=6), 1),
                 "fuseonly": round(r.run(T, "fuseonly", layers=6), 1),
-                "tokenweave": round(min(r.run(T, "tokenweave", prefix=a, boundary_sms=b, layers=6)
-                                        for b in (16, 32, 64)), 1),
+                "tokenweave_by_boundary_sms": {str(b): round(r.run(T, "tokenweave", prefix=a, boundary_sms=b,
+                                                                   layers=6), 1) for b in (16, 32, 64)},
                 "nocomm": round(r.run(T, "nocomm", layers=6), 1),
                 "cublas_version": r.cublas_version,
-                "note": "per-layer device time, eager launches; GEMMs are cuBLAS load (not product)"}
+                "note": "per-layer device time, eager launches, every boundary budget reported (none selected); "
+                        "GEMMs are cuBLAS load (not product); boundary op = K2 on one GPU"}
             r.close()
         except Exception as exc:  # libtw_weave / cuBLAS unavailable: report, do not fail the bench
             line["weave_llama70b_tp8_shapes_us"] = {"error": str(exc)[:200]}
         threads = os.cpu_count() or 1
-        sample_T = 2048
-        cpu_ms = reference_rmsnorm_ms(sample_T, H, threads, 3)
+        cpu_ms = reference_rmsnorm_each_ms(T, H, threads, 4)[1:]
         line["cpu_baseline"] = {
-            "value": round(1e3 * cpu_ms * T / sample_T, 1), "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"weavesim::rmsnorm_residual (oracle/_ref, reference sources compiled unmodified) on "
-                      f"{sample_T}x{H} fp32 rows over {threads} threads, median of 3, scaled x{T // sample_T}"}
+            "value": round(1e3 * statistics.median(cpu_ms), 1), "unit": UNIT, "cores": threads, "kind": "reference",
+            "cpu": cpu_model(),
+            "sample": f"full workload: weavesim::rmsnorm_residual (oracle/_ref, reference sources compiled "
+                      f"unmodified) on {T}x{H} fp32, token rows chunked over {threads} threads (as "
+                      f"--impl reference), median of 3 after one warm-up; ms {[round(x, 1) for x in cpu_ms]}"}
     line["wall_s"] = round(wall, 2)
     print(json.dumps(line), flush=True)
     return 0
+
+
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` without torchrun: spawn the N ranks ourselves
+    (same command line under torch.distributed.run, 127.0.0.1 rendezvous)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -400,15 +464,22 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--tokens", type=int, default=8192)
     ap.add_argument("--hidden", type=int, default=8192)
-    ap.add_argument("--sm-budget", type=int, default=16, help="K1 CTAs per rank (N>1)")
+    ap.add_argument("--sm-budget", type=int, default=8, help="K1 CTAs (= SMs) per rank (N>1)")
     ap.add_argument("--gather-residual", action="store_true", help="K1 G=2 (N>1)")
+    ap.add_argument("--transport", choices=["nvls", "peer", "auto"], default="nvls",
+                    help="N>1 on distinct GPUs: nvls (default; fail if unavailable), peer, or auto")
     ap.add_argument("--quick", action="store_true", help="skip sweeps/baselines (profiling runs)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
+    # our arm: the package loads the CUDA toolkit's cuBLAS before torch
+    # (paper_2505_11329_b200/_lib.py), so it is imported before anything else
+    import paper_2505_11329_b200  # noqa: F401
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         from tools.bench_tp import run_tp
         return run_tp(args)
+    if args.gpus > 1:
+        return relaunch_under_torchrun(args)
     return run_ours_single(args)
 
 

@@ -139,6 +139,24 @@ TW_API tw_status tw_weave_emulate_comm(tw_weave_t w, const int64_t* tokens, cons
 TW_API tw_status tw_weave_trace(tw_weave_t w, int max_events, int* n_events, int* op, int* split, int* stream,
                                 float* start_us, float* end_us);
 
+/* The runner's device buffers (bf16 unless noted), for tests that seed the
+ * layer's weights and read its activations back: the layer's state after a
+ * run is what the schedule computed, so two schedules of the same layers can
+ * be compared value for value.  HIDDEN is the buffer the current mode's
+ * boundary op writes ([max_tokens, H]; in TP mode the comm OUTPUT).
+ * *bytes receives the buffer's size. */
+typedef enum tw_weave_buf {
+  TW_WEAVE_BUF_HIDDEN = 0,     /* X  [max_tokens, H]                      */
+  TW_WEAVE_BUF_RESIDUAL = 1,   /* R  [max_tokens, H]                      */
+  TW_WEAVE_BUF_PARTIAL = 2,    /* P  [max_tokens, H] (GEMM partial sums)  */
+  TW_WEAVE_BUF_W_QKV = 3,      /* [H, qkv_width/tp]                       */
+  TW_WEAVE_BUF_W_O = 4,        /* [heads/tp * head_dim, H]                */
+  TW_WEAVE_BUF_W_UP = 5,       /* [experts][H, 2*I/tp]                    */
+  TW_WEAVE_BUF_W_DOWN = 6,     /* [experts][I/tp, H]                      */
+  TW_WEAVE_BUF_NORM_WEIGHT = 7 /* fp32 [H]                                */
+} tw_weave_buf;
+TW_API tw_status tw_weave_buffer(tw_weave_t w, tw_weave_buf which, void** ptr, size_t* bytes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -181,9 +181,9 @@ class RefLib:
         L.ref_smart_offset_analytic.restype = c_int64
         L.ref_make_split_plan.argtypes = [c_char_p, c_char_p, c_int64, _I64, _I64]
         L.ref_layer_latency.argtypes = [c_char_p, c_char_p, c_int64, c_char_p, POINTER(c_double)]
-        L.ref_time_fused.argtypes = [c_int, c_int64, c_int64, c_int, c_int, POINTER(c_double)]
+        L.ref_time_fused.argtypes = [c_int, c_int64, c_int64, c_int, c_int, POINTER(c_double), POINTER(c_double)]
         L.ref_calibrate_file.argtypes = [c_char_p, POINTER(c_double)]
-        L.ref_time_rmsnorm.argtypes = [c_int64, c_int64, c_int, c_int, POINTER(c_double)]
+        L.ref_time_rmsnorm.argtypes = [c_int64, c_int64, c_int, c_int, POINTER(c_double), POINTER(c_double)]
         _D = POINTER(c_double)
         L.ref_form_batches.argtypes = [_I64, _D, c_int64, c_int64, _I64, c_int64, _I64, c_int64, _I64]
         L.ref_save_trace.argtypes = [_I64, _D, c_int64, c_char_p]
@@ -284,19 +284,25 @@ class RefLib:
                 "hbm_bandwidth_effective", "fused_extra_latency_s")
         return dict(zip(keys, list(out)))
 
-    def time_fused(self, world, T, H, parallel, iters) -> float:
+    def time_fused(self, world, T, H, parallel, iters, each: bool = False):
+        """weavesim::fused_allreduce_rmsnorm timed `iters` times on one set of
+        inputs: the median (ms), or every iteration's time with each=True."""
         ms = c_double()
-        st = self.L.ref_time_fused(world, T, H, 1 if parallel else 0, iters, ctypes.byref(ms))
+        per = (c_double * max(iters, 1))()
+        st = self.L.ref_time_fused(world, T, H, 1 if parallel else 0, iters, ctypes.byref(ms), per)
         if st:
             raise StatusError(st, "ref_time_fused")
-        return ms.value
+        return list(per)[:iters] if each else ms.value
 
-    def time_rmsnorm(self, T, H, threads, iters) -> float:
+    def time_rmsnorm(self, T, H, threads, iters, each: bool = False):
+        """weavesim::rmsnorm_residual over T x H chunked across `threads` host
+        threads: the median (ms), or every iteration's time with each=True."""
         ms = c_double()
-        st = self.L.ref_time_rmsnorm(T, H, threads, iters, ctypes.byref(ms))
+        per = (c_double * max(iters, 1))()
+        st = self.L.ref_time_rmsnorm(T, H, threads, iters, ctypes.byref(ms), per)
         if st:
             raise StatusError(st, "ref_time_rmsnorm")
-        return ms.value
+        return list(per)[:iters] if each else ms.value
 
     @staticmethod
     def _req_arrays(requests):

@@ -235,8 +235,10 @@ int ref_calibrate_file(const char* path, double* out6) {
 // Times fused_allreduce_rmsnorm on a fixed group `iters` times; returns the
 // median milliseconds.  Residual shards are restored (outside the timed
 // region) before every call so each call sees the same inputs.
+// each_ms (optional, iters entries): every iteration's time, so a caller can
+// drop warm-up iterations without regenerating the inputs.
 int ref_time_fused(int world, std::int64_t T, std::int64_t H, int parallel, int iters,
-                   double* median_ms) {
+                   double* median_ms, double* each_ms) {
   return guarded([&] {
     RankGroup g;
     g.world_size = world;
@@ -263,6 +265,7 @@ int ref_time_fused(int world, std::int64_t T, std::int64_t H, int parallel, int 
       TokenMatrix out = fused_allreduce_rmsnorm(g, p, shards, parallel != 0);
       const auto t1 = std::chrono::steady_clock::now();
       ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+      if (each_ms) each_ms[i] = ms.back();
     }
     std::sort(ms.begin(), ms.end());
     *median_ms = ms[ms.size() / 2];
@@ -273,7 +276,8 @@ int ref_time_fused(int world, std::int64_t T, std::int64_t H, int parallel, int 
 // the reference rmsnorm_residual on a contiguous token chunk (the reference
 // op is single-threaded; chunking across cores is the caller-level
 // parallelism a host deployment would use).  Returns median milliseconds.
-int ref_time_rmsnorm(std::int64_t T, std::int64_t H, int threads, int iters, double* median_ms) {
+int ref_time_rmsnorm(std::int64_t T, std::int64_t H, int threads, int iters, double* median_ms,
+                     double* each_ms) {
   return guarded([&] {
     if (threads < 1) threads = 1;
     std::mt19937_64 rng(4321);
@@ -300,6 +304,7 @@ int ref_time_rmsnorm(std::int64_t T, std::int64_t H, int threads, int iters, dou
       for (auto& th : pool) th.join();
       const auto t1 = std::chrono::steady_clock::now();
       ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+      if (each_ms) each_ms[i] = ms.back();
     }
     std::sort(ms.begin(), ms.end());
     *median_ms = ms[ms.size() / 2];

@@ -244,6 +244,8 @@ void destroy_comm(tw_comm* c) {
     if (rb.phys) d.memRelease(rb.phys);
   }
   if (c->mc) d.memRelease(c->mc);
+  for (cudaEvent_t e : c->join)
+    if (e) cudaEventDestroy(e);
   delete c;
 }
 
@@ -738,7 +740,13 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
   p.row_offset = token_offset;
   p.eps = eps;
   // co-located ranks share one GPU: device-scope barrier fences suffice
-  p.flags = (flags & ~(kDeviceScope | kNvlsDepthMask)) | (comm->colocated ? kDeviceScope : 0u);
+  // (TW_FORCE_SYS_SCOPE=1 keeps system scope -- measurement of what the
+  // fences cost ranks on different GPUs, tools/k1_small.py)
+  static const bool force_sys = [] {
+    const char* e = std::getenv("TW_FORCE_SYS_SCOPE");
+    return e && e[0] == '1';
+  }();
+  p.flags = (flags & ~(kDeviceScope | kNvlsDepthMask)) | (comm->colocated && !force_sys ? kDeviceScope : 0u);
   p.world = W;
   // Barrier poll bound (~2 s at the default) and the fault-injection hook of
   // the timeout path: TW_FAULT_DROP_ARRIVAL_RANK=r makes rank r never signal,
@@ -775,8 +783,32 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
     for (int r = 0; r < W; ++r) fill_slot(p.slot[r], r);
     p.err = comm->ranks[0].err;
     cudaStream_t s = streams ? static_cast<cudaStream_t>(streams[0]) : nullptr;
+    // one grid for every rank on streams[0]; distinct per-rank streams are
+    // joined into it before the launch and released after it, so tw.h's
+    // "streams[r] is rank r's stream" ordering holds
+    bool distinct = false;
+    for (int r = 1; streams && r < W; ++r) distinct |= streams[r] != streams[0];
+    if (distinct) {
+      if (comm->join.empty()) {
+        comm->join.assign(W, nullptr);
+        for (int r = 0; r < W; ++r) {
+          cudaError_t e = cudaEventCreateWithFlags(&comm->join[r], cudaEventDisableTiming);
+          if (e != cudaSuccess) return cuda_fail(e, "comm: join events");
+        }
+      }
+      for (int r = 1; r < W; ++r) {
+        if (streams[r] == streams[0]) continue;
+        cudaEventRecord(comm->join[r], static_cast<cudaStream_t>(streams[r]));
+        cudaStreamWaitEvent(s, comm->join[r], 0);
+      }
+    }
     cudaError_t e = launch(p, dim3(budget, W), s);
     if (e != cudaSuccess) return cuda_fail(e, op);
+    if (distinct) {
+      cudaEventRecord(comm->join[0], s);
+      for (int r = 1; r < W; ++r)
+        if (streams[r] != streams[0]) cudaStreamWaitEvent(static_cast<cudaStream_t>(streams[r]), comm->join[0], 0);
+    }
   } else {
     for (int r = 0; r < W; ++r) {
       if (!owned(r)) continue;

@@ -23,6 +23,11 @@ struct HostIoCtx {
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
   cudaEvent_t loaded[kSlots] = {}, computed[kSlots] = {}, drained[kSlots] = {};
   cudaEvent_t start = nullptr, finish_c = nullptr, finish_d = nullptr;
+  // recorded on d2h after every call's last copy (d2h having joined comp):
+  // the next call's three streams wait on it, so a call issued on another
+  // caller stream cannot overwrite the weight or a staging slot the previous
+  // call is still reading (the mutex only serialises enqueueing)
+  cudaEvent_t done = nullptr;
   void* buf[kSlots][4] = {};  // in, res, out, res_out per slot
   void* weight = nullptr;
   size_t weight_bytes = 0;
@@ -42,7 +47,7 @@ tw_status ensure(HostIoCtx& c, int dev, size_t chunk_bytes, size_t wbytes) {
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.computed[i], cudaEventDisableTiming);
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c.drained[i], cudaEventDisableTiming);
     }
-    for (cudaEvent_t* ev : {&c.start, &c.finish_c, &c.finish_d})
+    for (cudaEvent_t* ev : {&c.start, &c.finish_c, &c.finish_d, &c.done})
       if (e == cudaSuccess) e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
     if (e != cudaSuccess) return cuda_fail(e, "host_io: streams/events");
   }
@@ -103,7 +108,10 @@ tw_status tw_rmsnorm_residual_host(const void* h_input, const void* h_residual, 
   cudaStream_t caller = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaEventRecord(c.start, caller);
   if (e != cudaSuccess) return cuda_fail(e, "host_io: record");
-  for (cudaStream_t s : {c.h2d, c.comp, c.d2h}) cudaStreamWaitEvent(s, c.start, 0);
+  for (cudaStream_t s : {c.h2d, c.comp, c.d2h}) {
+    cudaStreamWaitEvent(s, c.start, 0);
+    cudaStreamWaitEvent(s, c.done, 0);  // the previous call on this device (no-op before the first)
+  }
   e = cudaMemcpyAsync(c.weight, h_weight, H * sizeof(float), cudaMemcpyHostToDevice, c.h2d);
   if (e != cudaSuccess) return cuda_fail(e, "host_io: weight H2D");
   const char* hin = static_cast<const char*>(h_input);
@@ -136,6 +144,8 @@ tw_status tw_rmsnorm_residual_host(const void* h_input, const void* h_residual, 
   }
   cudaEventRecord(c.finish_c, c.comp);
   cudaEventRecord(c.finish_d, c.d2h);
+  cudaStreamWaitEvent(c.d2h, c.finish_c, 0);
+  cudaEventRecord(c.done, c.d2h);
   cudaStreamWaitEvent(caller, c.finish_c, 0);
   cudaStreamWaitEvent(caller, c.finish_d, 0);
   return TW_OK;

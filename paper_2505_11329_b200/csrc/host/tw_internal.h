@@ -72,6 +72,9 @@ struct tw_comm {
   std::vector<tw::RankBuffers> ranks;
   CUmemGenericAllocationHandle mc = 0;
   int local_rank = -1;      // >= 0: multi-process communicator owning only this rank
+  // co-located launches go on streams[0]: these join the other ranks' streams
+  // before (rank r's event) and after (slot 0) the launch
+  std::vector<cudaEvent_t> join;
 };
 
 namespace tw {

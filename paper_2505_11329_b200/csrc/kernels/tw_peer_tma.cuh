@@ -75,6 +75,9 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
 
   if (warp == 0) {
     if (lane == 0) {
+      // The entry barrier acquired the peers' INPUT writes through the generic
+      // proxy; the bulk loads below read them through the async proxy.
+      asm volatile("fence.proxy.async.global;" ::: "memory");
       long long g = 0;  // stage sequence number
       for (long long i = 0; i < nrows; ++i) {
         const long long t = row0 + blockIdx.x + i * stride;
@@ -214,12 +217,14 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
       }
     }
     if (storer) {
-      bulk_wait_all();  // every store performed before the exit barrier signals
+      // Every bulk store performed, then ordered (async -> generic proxy)
+      // before this thread's later operations.  No scope fence here: the
+      // exit barrier's bar.sync puts these writes before thread 0's
+      // fence.acq_rel + red (release pattern, cumulative over the CTA), so
+      // one fence per CTA exit publishes them (a second fence here cost a
+      // system-scope fence per CTA on the critical path).
+      bulk_wait_all();
       asm volatile("fence.proxy.async.global;" ::: "memory");
-      if (p.flags & kDeviceScope)
-        fence_acq_rel_gpu();
-      else
-        fence_acq_rel_sys();
     }
   }
   rank_barrier<Xport::Peer>(p, s, 2);

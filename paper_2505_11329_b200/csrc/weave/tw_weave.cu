@@ -524,6 +524,26 @@ static tw_status weave_create(const tw_layer_spec* spec, int64_t max_tokens, int
   return TW_OK;
 }
 
+tw_status tw_weave_buffer(tw_weave_t w, tw_weave_buf which, void** ptr, size_t* bytes) {
+  if (!w || !ptr) return werr(TW_ERR_CONFIG, "weave_buffer: null argument");
+  const tw_layer_spec& sp = w->spec;
+  const int64_t H = sp.hidden, T = w->max_tokens, I = sp.intermediate / sp.tp;
+  size_t n = 0;
+  switch (which) {
+    case TW_WEAVE_BUF_HIDDEN: *ptr = w->X; n = size_t(T * H * kBf16); break;
+    case TW_WEAVE_BUF_RESIDUAL: *ptr = w->R; n = size_t(T * H * kBf16); break;
+    case TW_WEAVE_BUF_PARTIAL: *ptr = w->P; n = size_t(T * H * kBf16); break;
+    case TW_WEAVE_BUF_W_QKV: *ptr = w->Wqkv; n = size_t(H * w->qkvw * kBf16); break;
+    case TW_WEAVE_BUF_W_O: *ptr = w->Wo; n = size_t(w->hg * sp.head_dim * H * kBf16); break;
+    case TW_WEAVE_BUF_W_UP: *ptr = w->Wup; n = size_t(sp.experts * H * 2 * I * kBf16); break;
+    case TW_WEAVE_BUF_W_DOWN: *ptr = w->Wdown; n = size_t(sp.experts * I * H * kBf16); break;
+    case TW_WEAVE_BUF_NORM_WEIGHT: *ptr = w->wnorm; n = size_t(H * sizeof(float)); break;
+    default: return werr(TW_ERR_CONFIG, "weave_buffer: unknown buffer");
+  }
+  if (bytes) *bytes = n;
+  return TW_OK;
+}
+
 tw_status tw_weave_destroy(tw_weave_t w) {
   if (!w) return TW_OK;
   cudaSetDevice(w->device);

@@ -205,7 +205,8 @@ def _weave_lib():
     lib.tw_weave_last_error.argtypes = []
     lib.tw_weave_trace.argtypes = [c_void_p, c_int, POINTER(c_int), POINTER(c_int), POINTER(c_int), POINTER(c_int),
                                    POINTER(c_float), POINTER(c_float)]
-    for f in ("tw_weave_create", "tw_weave_destroy", "tw_weave_run", "tw_weave_trace"):
+    lib.tw_weave_buffer.argtypes = [c_void_p, c_int, POINTER(c_void_p), POINTER(ctypes.c_size_t)]
+    for f in ("tw_weave_create", "tw_weave_destroy", "tw_weave_run", "tw_weave_trace", "tw_weave_buffer"):
         getattr(lib, f).restype = c_int
     return lib
 
@@ -301,3 +302,18 @@ class LayerRunner:
         self._check(self._L.tw_weave_trace(self._h, max_events, ctypes.byref(n), op, sp, st, a, b))
         return [{"op": OPS[op[i]], "split": SPLITS[sp[i]], "stream": "comm" if st[i] else "compute",
                  "start_us": a[i], "end_us": b[i]} for i in range(n.value)]
+
+    BUFFERS = {"hidden": 0, "residual": 1, "partial": 2, "w_qkv": 3, "w_o": 4, "w_up": 5, "w_down": 6,
+               "norm_weight": 7}
+
+    def buffer(self, which: str):
+        """torch view (no copy) of one of the runner's device buffers
+        (tw_weave_buffer): bf16 1-D, or fp32 for "norm_weight"."""
+        import torch
+        from . import _DevBuf
+        p, nb = c_void_p(), ctypes.c_size_t()
+        self._check(self._L.tw_weave_buffer(self._h, self.BUFFERS[which], ctypes.byref(p), ctypes.byref(nb)))
+        if which == "norm_weight":
+            return torch.as_tensor(_DevBuf(p.value, (nb.value // 4,), "<f4"), device="cuda")
+        raw = torch.as_tensor(_DevBuf(p.value, (nb.value // 2,), "<i2"), device="cuda")
+        return raw.view(torch.bfloat16)

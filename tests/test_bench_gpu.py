@@ -40,6 +40,12 @@ def test_bench_single_gpu_line():
     assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+    assert "full workload" in cb["sample"]
+    # the reference's own C++ API and dtype through the drop-in (same config as --impl reference)
+    f32 = d["e2e_dropin_f32"]
+    assert f32["dtype"] == "f32" and f32["value"] > 0 and f32["h2d_bytes_per_step"] > 0, f32
+    assert d["kernel_us"]["back_to_back_no_flush"] > 0
+    assert set(d["weave_llama70b_tp8_shapes_us"]["tokenweave_by_boundary_sms"]) == {"16", "32", "64"}
 
 
 @pytest.mark.gpu
@@ -61,3 +67,17 @@ def test_bench_torchrun_two_ranks():
               "--tokens", "1024"], env={"TW_BARRIER_SPIN_LIMIT": str(1 << 28)})
     assert d["n_gpus"] == 2 and BASE_KEYS <= set(d) and d["value"] > 0
     assert d["roofline"]["bound"] in ("nvlink", "hbm")
+    # one GPU: the two ranks are co-located (PEER), and the line says so
+    assert d["config"]["colocated"] is True and d["config"]["transport"] == "peer"
+    assert d["config"]["sm_budget"] == 8 and d["sms_consumed"] == 8
+    assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0
+    assert {"sm_mhz", "reasons"} <= set(d["clocks"])
+    assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] == 2
+
+
+@pytest.mark.gpu
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` without torchrun launches the two ranks itself."""
+    d = _run([sys.executable, "bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--tokens", "1024",
+              "--quick"], env={"TW_BARRIER_SPIN_LIMIT": str(1 << 28)})
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["tp"] == 2

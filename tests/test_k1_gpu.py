@@ -58,7 +58,7 @@ def oracle_case(orc, inputs, residual, weight, ranges, bf16):
     return inputs, residual, out, new
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 @pytest.mark.parametrize("T", [1, 3, 17, 40, 256])
 @pytest.mark.parametrize("H", [16, 24, 33, 64, 1024])
 def test_k1_fp32_matches_oracle(cuda, orc, world, T, H):
@@ -74,7 +74,7 @@ def test_k1_fp32_matches_oracle(cuda, orc, world, T, H):
         assert np.array_equal(outs[r], outs[0]), "replicated output must be identical on every rank"
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("world", [2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("T,H", [(1, 16), (17, 64), (40, 33), (256, 1024), (128, 8192), (64, 6144)])
 def test_k1_bf16_matches_oracle(cuda, orc, world, T, H):
     import torch

@@ -1,0 +1,115 @@
+// dropin_bench.cpp -- times the reference's own C++ operator API, as a
+// reference user calls it, linked against the B200 drop-in
+// (libweavesim_b200.so) instead of the reference library:
+//
+//   dropin_bench rmsnorm T H warmup steps
+//       weavesim::rmsnorm_residual(TokenMatrix, TokenMatrix, NormParams)
+//       (proj/include/weavesim/numerics.hpp:42-43): fp32 host matrices in,
+//       fp32 host matrices out, validation included -- the reference's dtype
+//       and call, so the ratio against `bench.py --impl reference` (the same
+//       function from the reference sources on the host cores) is like for
+//       like.
+//   dropin_bench fused N T H warmup steps
+//       weavesim::fused_allreduce_rmsnorm(RankGroup&, NormParams, ShardMap)
+//       (proj/include/weavesim/collectives.hpp:63-64) with N ranks.
+//
+// Prints one JSON object: per-step wall milliseconds (std::chrono around the
+// call; the API is synchronous, so host<->device copies are inside).
+// Inputs: U(-1,1) from std::mt19937_64, weight 1 (the reference arm's
+// oracle/ref_capi.cpp ref_time_* draws).
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "weavesim/collectives.hpp"
+#include "weavesim/numerics.hpp"
+
+using namespace weavesim;
+
+namespace {
+
+void fill(TokenMatrix& m, std::mt19937_64& rng) {
+  std::uniform_real_distribution<float> dist(-1.0f, 1.0f);
+  for (float& v : m.values) v = dist(rng);
+}
+
+void emit(const char* op, const std::vector<double>& ms, std::int64_t bytes_in, std::int64_t bytes_out) {
+  std::vector<double> s = ms;
+  std::sort(s.begin(), s.end());
+  double sum = 0;
+  for (double v : ms) sum += v;
+  std::printf("{\"op\": \"%s\", \"median_ms\": %.4f, \"mean_ms\": %.4f, \"min_ms\": %.4f, \"max_ms\": %.4f, "
+              "\"h2d_bytes\": %lld, \"d2h_bytes\": %lld, \"each_ms\": [",
+              op, s[s.size() / 2], sum / ms.size(), s.front(), s.back(), static_cast<long long>(bytes_in),
+              static_cast<long long>(bytes_out));
+  for (size_t i = 0; i < ms.size(); ++i) std::printf("%s%.4f", i ? ", " : "", ms[i]);
+  std::printf("]}\n");
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::fprintf(stderr, "usage: dropin_bench rmsnorm T H warmup steps | fused N T H warmup steps\n");
+    return 2;
+  }
+  const std::string op = argv[1];
+  std::mt19937_64 rng(4321);
+  NormParams p;
+  if (op == "rmsnorm" && argc == 6) {
+    const std::int64_t T = std::atoll(argv[2]), H = std::atoll(argv[3]);
+    const int warmup = std::atoi(argv[4]), steps = std::atoi(argv[5]);
+    TokenMatrix in = TokenMatrix::zeros(T, H), res = TokenMatrix::zeros(T, H);
+    fill(in, rng);
+    fill(res, rng);
+    p.weight.assign(static_cast<size_t>(H), 1.0f);
+    std::vector<double> ms;
+    for (int i = 0; i < warmup + steps; ++i) {
+      const auto t0 = std::chrono::steady_clock::now();
+      NormResult r = rmsnorm_residual(in, res, p);
+      const auto t1 = std::chrono::steady_clock::now();
+      if (i >= warmup) ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+      if (r.output.values.size() != in.values.size()) return 1;
+    }
+    const std::int64_t nb = T * H * 4;
+    emit("rmsnorm_residual", ms, 2 * nb + H * 4, 2 * nb);
+    return 0;
+  }
+  if (op == "fused" && argc == 7) {
+    const int N = std::atoi(argv[2]);
+    const std::int64_t T = std::atoll(argv[3]), H = std::atoll(argv[4]);
+    const int warmup = std::atoi(argv[5]), steps = std::atoi(argv[6]);
+    RankGroup g;
+    g.world_size = N;
+    for (int r = 0; r < N; ++r) {
+      g.inputs.push_back(TokenMatrix::zeros(T, H));
+      fill(g.inputs.back(), rng);
+    }
+    const ShardMap shards = token_shard_map(T, N);
+    for (const TokenRange& range : shards.ranges) {
+      g.residual_shards.push_back(TokenMatrix::zeros(range.size(), H));
+      fill(g.residual_shards.back(), rng);
+    }
+    p.weight.assign(static_cast<size_t>(H), 1.0f);
+    const std::vector<TokenMatrix> saved = g.residual_shards;
+    std::vector<double> ms;
+    for (int i = 0; i < warmup + steps; ++i) {
+      g.residual_shards = saved;
+      const auto t0 = std::chrono::steady_clock::now();
+      TokenMatrix out = fused_allreduce_rmsnorm(g, p, shards, true);
+      const auto t1 = std::chrono::steady_clock::now();
+      if (i >= warmup) ms.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+      if (out.values.size() != static_cast<size_t>(T * H)) return 1;
+    }
+    const std::int64_t nb = T * H * 4;
+    emit("fused_allreduce_rmsnorm", ms, N * nb + nb + N * H * 4, 2 * nb);
+    return 0;
+  }
+  std::fprintf(stderr, "bad arguments\n");
+  return 2;
+}

@@ -4,7 +4,9 @@ per T.  Median of CUDA-event times over back-to-back launches (no flush: the
 working set is L2-resident at these sizes), eager and replayed from a CUDA
 graph.  An HBM/L2-bound stand-in for the NVLink case, not an NVLink number.
 
-    python tools/k1_small.py [--out profiles/k1_small_r01.json]
+    python tools/k1_small.py [--transport peer|nvls_sim] [--out FILE]
+    TW_FORCE_SYS_SCOPE=1 python tools/k1_small.py ...   # system-scope barriers
+                                                         # (what ranks on different GPUs pay)
 """
 import argparse
 import json
@@ -36,12 +38,14 @@ def median_us(fn, reps=200):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default="")
+    ap.add_argument("--transport", choices=["peer", "nvls_sim"], default="peer")
     args = ap.parse_args()
     H = 8192
     rows = []
     for W in (2, 4, 8):
         Tmax = 256
-        comm = tw.Communicator(W, [0] * W, Tmax * H * 2, tw.TW_TRANSPORT_PEER)
+        tr = tw.TW_TRANSPORT_PEER if args.transport == "peer" else tw.TW_TRANSPORT_NVLS_SIM
+        comm = tw.Communicator(W, [0] * W, Tmax * H * 2, tr)
         for q in range(W):
             comm.buffer(q, tw.TW_BUF_INPUT, (Tmax, H), torch.bfloat16).normal_()
         w = [torch.ones(H, device="cuda")] * W
@@ -60,7 +64,9 @@ def main():
                         comm.fused_allreduce_rmsnorm(T, H, shards, w, sm_budget=budget)
             torch.cuda.current_stream().wait_stream(s)
             graph10 = median_us(g.replay, reps=50)
-            row = {"tp": W, "T": T, "sm_budget_per_rank": budget, "eager_us": eager,
+            row = {"tp": W, "T": T, "transport": args.transport,
+                   "barrier_scope": "system" if os.environ.get("TW_FORCE_SYS_SCOPE") == "1" else "device",
+                   "sm_budget_per_rank": budget, "eager_us": eager,
                    "graph_us_per_op": round(graph10 / 10, 2)}
             print(json.dumps(row), flush=True)
             rows.append(row)
