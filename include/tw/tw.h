@@ -113,6 +113,20 @@ TW_API tw_status tw_rmsnorm_residual_host(const void* h_input, const void* h_res
                                           void* h_output, const float* h_weight, int64_t T, int64_t H, float eps,
                                           tw_dtype dtype, int64_t chunk_rows, void* stream);
 
+/* Synchronous form for ANY host memory (pageable or pinned), the drop-in's
+ * std::vector path: chunks are staged through a pinned ring by a pool of host
+ * threads (copy-in of chunk k+1 | H2D | K2 | D2H | copy-out of chunk k-R
+ * overlapped), so pageable matrices are not moved by the driver's serial
+ * staging.  flags & TW_HOST_CHECK_FINITE: the staging copy also scans the
+ * input and residual for NaN/Inf and the call returns TW_ERR_NUMERIC
+ * ("TokenMatrix contains NaN/Inf") -- TokenMatrix::validate's check
+ * (proj/src/numerics.cpp:25-27) at no extra pass; the outputs are then
+ * unspecified.  Returns when the outputs are written. */
+#define TW_HOST_CHECK_FINITE 0x1u
+TW_API tw_status tw_rmsnorm_residual_host_sync(const void* h_input, const void* h_residual, void* h_residual_out,
+                                               void* h_output, const float* h_weight, int64_t T, int64_t H,
+                                               float eps, tw_dtype dtype, unsigned flags);
+
 /* Device-side finite scan: *nonfinite_count (device int32) += #NaN/Inf in x.
  * Replaces TokenMatrix::validate's isfinite loop (numerics.cpp:25-27). */
 TW_API tw_status tw_count_nonfinite(const void* x, int64_t n, tw_dtype dtype, int* nonfinite_count_dev, void* stream);
@@ -122,6 +136,11 @@ TW_API tw_status tw_count_nonfinite(const void* x, int64_t n, tw_dtype dtype, in
  * ShardMap::validate (:14-24).  ranges: 2*world int64 {begin,end}. */
 TW_API tw_status tw_token_shard_map(int64_t num_tokens, int world, int64_t* ranges);
 TW_API tw_status tw_shard_map_validate(const int64_t* ranges, int world, int64_t total_tokens);
+
+/* Ranks per communicator (the K1/K3 kernels carry every rank's pointers in
+ * their launch parameters).  The drop-in C++ API serves wider RankGroups by a
+ * chain of K2 launches (weavesim_dropin.cpp); the reference accepts any N >= 2. */
+#define TW_MAX_RANKS 8
 
 /* --- Communicator --------------------------------------------------------------
  * One communicator = `world` ranks with symmetric INPUT/OUTPUT/RESIDUAL buffers

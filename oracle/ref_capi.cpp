@@ -8,6 +8,7 @@
 // DimensionError 1, NumericError 2, ConfigError 3, ContractError 4, other 9.
 #include <algorithm>
 #include <chrono>
+#include <malloc.h>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -239,6 +240,8 @@ int ref_calibrate_file(const char* path, double* out6) {
 // drop warm-up iterations without regenerating the inputs.
 int ref_time_fused(int world, std::int64_t T, std::int64_t H, int parallel, int iters,
                    double* median_ms, double* each_ms) {
+  mallopt(M_MMAP_MAX, 0);  // heap reuse across iterations (see ref_time_rmsnorm)
+  mallopt(M_TRIM_THRESHOLD, 1 << 30);
   return guarded([&] {
     RankGroup g;
     g.world_size = world;
@@ -278,6 +281,9 @@ int ref_time_fused(int world, std::int64_t T, std::int64_t H, int parallel, int 
 // parallelism a host deployment would use).  Returns median milliseconds.
 int ref_time_rmsnorm(std::int64_t T, std::int64_t H, int threads, int iters, double* median_ms,
                      double* each_ms) {
+  // heap reuse across iterations, as tools/dropin_bench.cpp (the drop-in arm) sets
+  mallopt(M_MMAP_MAX, 0);
+  mallopt(M_TRIM_THRESHOLD, 1 << 30);
   return guarded([&] {
     if (threads < 1) threads = 1;
     std::mt19937_64 rng(4321);

@@ -18,6 +18,7 @@ TW_OK, TW_ERR_DIMENSION, TW_ERR_NUMERIC, TW_ERR_CONFIG, TW_ERR_CONTRACT, TW_ERR_
 TW_BF16, TW_F32 = 0, 1
 TW_TRANSPORT_AUTO, TW_TRANSPORT_NVLS, TW_TRANSPORT_PEER, TW_TRANSPORT_NVLS_SIM = 0, 1, 2, 3
 TW_BUF_INPUT, TW_BUF_OUTPUT, TW_BUF_RESIDUAL = 0, 1, 2
+TW_HOST_CHECK_FINITE = 0x1
 TW_GATHER_RESIDUAL = 0x1
 TRANSPORT_NAMES = {TW_TRANSPORT_AUTO: "auto", TW_TRANSPORT_NVLS: "nvls", TW_TRANSPORT_PEER: "peer",
                    TW_TRANSPORT_NVLS_SIM: "nvls_sim"}
@@ -85,6 +86,8 @@ _SIGNATURES = [
      [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_int, c_int, c_void_p]),
     ("tw_rmsnorm_residual_host", c_int,
      [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_int, c_int64, c_void_p]),
+    ("tw_rmsnorm_residual_host_sync", c_int,
+     [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_int, c_uint]),
     ("tw_count_nonfinite", c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p]),
     ("tw_token_shard_map", c_int, [c_int64, c_int, POINTER(c_int64)]),
     ("tw_shard_map_validate", c_int, [POINTER(c_int64), c_int, c_int64]),

@@ -746,7 +746,12 @@ tw_status comm_launch(tw_comm_t comm, int64_t T, int64_t H, int64_t token_offset
     const char* e = std::getenv("TW_FORCE_SYS_SCOPE");
     return e && e[0] == '1';
   }();
-  p.flags = (flags & ~(kDeviceScope | kNvlsDepthMask)) | (comm->colocated && !force_sys ? kDeviceScope : 0u);
+  static const bool alias_fence = [] {
+    const char* e = std::getenv("TW_NVLS_ALIAS_FENCE");
+    return e && e[0] == '1';
+  }();
+  p.flags = (flags & ~(kDeviceScope | kNvlsDepthMask | kAliasFence)) |
+            (comm->colocated && !force_sys ? kDeviceScope : 0u) | (alias_fence ? kAliasFence : 0u);
   p.world = W;
   // Barrier poll bound (~2 s at the default) and the fault-injection hook of
   // the timeout path: TW_FAULT_DROP_ARRIVAL_RANK=r makes rank r never signal,

@@ -152,3 +152,245 @@ tw_status tw_rmsnorm_residual_host(const void* h_input, const void* h_residual, 
 }
 
 }  // extern "C"
+
+// ---- synchronous path for pageable host memory (the drop-in's std::vectors) --------
+//
+// cudaMemcpyAsync from pageable memory is staged by the driver one piece at a
+// time on the calling thread (~5-10 GB/s, and it serialises the pipeline
+// above).  Here a pool of host threads copies each chunk between the caller's
+// memory and a pinned ring (scanning for NaN/Inf on the way in when asked),
+// and the copy engines move only pinned memory:
+//
+//   iteration k:  [host] copy-out chunk k-R (after its D2H) ; copy-in chunk k
+//                 [gpu ] H2D k | K2 k | D2H k   (three streams, as above)
+//
+// so the host copies of one chunk overlap the DMA and the kernel of the others.
+
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <thread>
+#include <vector>
+
+namespace tw {
+namespace {
+
+// Fixed pool; run(n, f) calls f(0..n-1) across the workers and the caller.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();  // never destroyed (threads detached at exit)
+    return *p;
+  }
+  int size() const { return static_cast<int>(threads_.size()) + 1; }
+  void run(int n, const std::function<void(int)>& f) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &f;
+      n_ = n;
+      next_.store(0);
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ == static_cast<int>(threads_.size()); });
+    job_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    // every hardware thread (the caller is one of them): the staging copies
+    // are host-memory-bandwidth work and the caller blocks on them
+    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    const int workers = static_cast<int>(std::min(32u, hw)) - 1;
+    for (int i = 0; i < std::max(0, workers); ++i)
+      threads_.emplace_back([this] { loop(); });
+    for (auto& t : threads_) t.detach();
+  }
+  void work() {
+    for (int i = next_.fetch_add(1); i < n_; i = next_.fetch_add(1)) (*job_)(i);
+  }
+  void loop() {
+    unsigned seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+      }
+      work();
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        ++done_;
+      }
+      done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* job_ = nullptr;
+  int n_ = 0, done_ = 0;
+  unsigned gen_ = 0;
+  std::atomic<int> next_{0};
+};
+
+// Copy `bytes` and report whether any element is NaN/Inf (exponent all ones).
+bool copy_check(void* dst, const void* src, size_t bytes, bool bf16, bool check) {
+  std::memcpy(dst, src, bytes);
+  if (!check) return false;
+  if (bf16) {
+    const uint16_t* v = static_cast<const uint16_t*>(dst);
+    uint32_t bad = 0;
+    for (size_t i = 0, n = bytes / 2; i < n; ++i) bad |= (v[i] & 0x7F80u) == 0x7F80u;
+    return bad != 0;
+  }
+  const uint32_t* v = static_cast<const uint32_t*>(dst);
+  uint32_t bad = 0;
+  for (size_t i = 0, n = bytes / 4; i < n; ++i) bad |= (v[i] & 0x7F800000u) == 0x7F800000u;
+  return bad != 0;
+}
+
+struct PinnedRing {
+  int device = -1;
+  size_t chunk = 0;
+  void* h[kSlots][4] = {};  // pinned in, res, out, res_out
+  cudaEvent_t drained[kSlots] = {};
+};
+PinnedRing g_ring[64];
+
+tw_status ensure_ring(PinnedRing& g, int dev, size_t chunk) {
+  if (g.device != dev) {
+    g.device = dev;
+    for (int i = 0; i < kSlots; ++i) {
+      cudaError_t e = cudaEventCreateWithFlags(&g.drained[i], cudaEventDisableTiming);
+      if (e != cudaSuccess) return cuda_fail(e, "host_sync: events");
+    }
+  }
+  if (g.chunk < chunk) {
+    for (int i = 0; i < kSlots; ++i)
+      for (int j = 0; j < 4; ++j) {
+        if (g.h[i][j]) cudaFreeHost(g.h[i][j]);
+        g.h[i][j] = nullptr;
+        cudaError_t e = cudaHostAlloc(&g.h[i][j], chunk, cudaHostAllocDefault);
+        if (e != cudaSuccess) {
+          g.chunk = 0;
+          return cuda_fail(e, "host_sync: cudaHostAlloc");
+        }
+      }
+    g.chunk = chunk;
+  }
+  return TW_OK;
+}
+
+}  // namespace
+}  // namespace tw
+
+extern "C" {
+
+tw_status tw_rmsnorm_residual_host_sync(const void* h_input, const void* h_residual, void* h_residual_out,
+                                        void* h_output, const float* h_weight, int64_t T, int64_t H, float eps,
+                                        tw_dtype dtype, unsigned flags) {
+  clear_error();
+  if (T < 0 || H < 1) return fail(TW_ERR_DIMENSION, "rmsnorm_residual_host_sync: requires T >= 0 and H >= 1");
+  if (!(eps > 0.0f) && eps != 0.0f)
+    return fail(TW_ERR_NUMERIC, "rmsnorm_residual_host_sync: epsilon must be nonnegative");
+  if (dtype != TW_BF16 && dtype != TW_F32) return fail(TW_ERR_CONFIG, "rmsnorm_residual_host_sync: unknown dtype");
+  if (T == 0) return TW_OK;
+  if (!h_input || !h_residual || !h_residual_out || !h_output || !h_weight)
+    return fail(TW_ERR_DIMENSION, "rmsnorm_residual_host_sync: null buffer");
+  const bool bf16 = dtype == TW_BF16;
+  const bool check = flags & TW_HOST_CHECK_FINITE;
+  const size_t row = static_cast<size_t>(H) * (bf16 ? 2 : 4);
+  const int64_t chunk_rows = std::min<int64_t>(T, std::max<int64_t>(1, static_cast<int64_t>((8u << 20) / row)));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return fail(TW_ERR_CONFIG, "rmsnorm_residual_host_sync: device index");
+  std::lock_guard<std::mutex> lock(g_mu);
+  HostIoCtx& c = g_ctx[dev];
+  PinnedRing& g = g_ring[dev];
+  const size_t cb = static_cast<size_t>(chunk_rows) * row;
+  tw_status st = ensure(c, dev, cb, static_cast<size_t>(H) * sizeof(float));
+  if (st == TW_OK) st = ensure_ring(g, dev, cb);
+  if (st != TW_OK) return st;
+  cudaError_t e = cudaSuccess;
+  for (cudaStream_t s : {c.h2d, c.comp, c.d2h}) cudaStreamWaitEvent(s, c.done, 0);
+  e = cudaMemcpyAsync(c.weight, h_weight, H * sizeof(float), cudaMemcpyHostToDevice, c.h2d);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c.h2d);  // h_weight may be pageable and short-lived
+  if (e != cudaSuccess) return cuda_fail(e, "host_sync: weight H2D");
+  HostPool& pool = HostPool::get();
+  const int parts = pool.size();
+  const char* hin = static_cast<const char*>(h_input);
+  const char* hres = static_cast<const char*>(h_residual);
+  char* hro = static_cast<char*>(h_residual_out);
+  char* hout = static_cast<char*>(h_output);
+  const int64_t K = (T + chunk_rows - 1) / chunk_rows;
+  auto span = [&](int64_t k, size_t* off, size_t* nb) {
+    const int64_t r0 = k * chunk_rows, n = std::min(chunk_rows, T - r0);
+    *off = static_cast<size_t>(r0) * row;
+    *nb = static_cast<size_t>(n) * row;
+  };
+  // parallel copy of one chunk's two matrices, split in `parts` x 2 pieces
+  auto pcopy = [&](char* d0, const char* s0, char* d1, const char* s1, size_t nb, bool chk) {
+    std::atomic<bool> bad{false};
+    const size_t elem = bf16 ? 2 : 4;
+    const size_t piece = ((nb / elem + parts - 1) / parts) * elem;
+    pool.run(2 * parts, [&](int i) {
+      const int m = i / parts;
+      const size_t a = static_cast<size_t>(i % parts) * piece;
+      if (a >= nb) return;
+      const size_t n = std::min(piece, nb - a);
+      if (copy_check((m ? d1 : d0) + a, (m ? s1 : s0) + a, n, bf16, chk)) bad.store(true);
+    });
+    return bad.load();
+  };
+  auto copy_out = [&](int64_t k) -> tw_status {
+    const int s = static_cast<int>(k % kSlots);
+    cudaError_t ee = cudaEventSynchronize(g.drained[s]);
+    if (ee != cudaSuccess) return cuda_fail(ee, "host_sync: D2H");
+    size_t off, nb;
+    span(k, &off, &nb);
+    pcopy(hout + off, static_cast<const char*>(g.h[s][2]), hro + off, static_cast<const char*>(g.h[s][3]), nb,
+          false);
+    return TW_OK;
+  };
+  bool nonfinite = false;
+  for (int64_t k = 0; k < K && !nonfinite; ++k) {
+    const int s = static_cast<int>(k % kSlots);
+    if (k >= kSlots && (st = copy_out(k - kSlots)) != TW_OK) return st;  // also frees slot s's pinned in/out
+    size_t off, nb;
+    span(k, &off, &nb);
+    const int64_t n = static_cast<int64_t>(nb / row);
+    if (pcopy(static_cast<char*>(g.h[s][0]), hin + off, static_cast<char*>(g.h[s][1]), hres + off, nb, check)) {
+      nonfinite = true;
+      break;
+    }
+    void** b = c.buf[s];
+    if ((e = cudaMemcpyAsync(b[0], g.h[s][0], nb, cudaMemcpyHostToDevice, c.h2d)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(b[1], g.h[s][1], nb, cudaMemcpyHostToDevice, c.h2d)) != cudaSuccess)
+      return cuda_fail(e, "host_sync: H2D");
+    cudaEventRecord(c.loaded[s], c.h2d);
+    cudaStreamWaitEvent(c.comp, c.loaded[s], 0);
+    // (slot s's previous chunk, k - kSlots, was drained: copy_out synchronised on it)
+    st = tw_rmsnorm_residual(b[0], b[1], b[3], b[2], static_cast<const float*>(c.weight), n, H, eps, dtype, 0, c.comp);
+    if (st != TW_OK) return st;
+    cudaEventRecord(c.computed[s], c.comp);
+    cudaStreamWaitEvent(c.d2h, c.computed[s], 0);
+    if ((e = cudaMemcpyAsync(g.h[s][2], b[2], nb, cudaMemcpyDeviceToHost, c.d2h)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(g.h[s][3], b[3], nb, cudaMemcpyDeviceToHost, c.d2h)) != cudaSuccess)
+      return cuda_fail(e, "host_sync: D2H");
+    cudaEventRecord(g.drained[s], c.d2h);
+  }
+  if (nonfinite) {
+    for (cudaStream_t q : {c.h2d, c.comp, c.d2h}) cudaStreamSynchronize(q);
+    return fail(TW_ERR_NUMERIC, "TokenMatrix contains NaN/Inf");
+  }
+  for (int64_t k = std::max<int64_t>(0, K - kSlots); k < K; ++k)
+    if ((st = copy_out(k)) != TW_OK) return st;
+  cudaEventRecord(c.done, c.d2h);  // every chunk drained (copy_out synchronised on each)
+  return TW_OK;
+}
+
+}  // extern "C"

@@ -140,26 +140,43 @@ void TokenMatrix::validate() const {
 }
 
 NormResult rmsnorm_residual(const TokenMatrix& input, const TokenMatrix& residual, const NormParams& params) {
-  input.validate();
-  residual.validate();
-  if (!input.same_shape(residual)) throw DimensionError("rmsnorm_residual: input and residual shapes differ");
-  if (static_cast<std::int64_t>(params.weight.size()) != input.hidden)
-    throw DimensionError("rmsnorm_residual: weight length must equal hidden size");
-  if (!(params.epsilon > 0.0f) && params.epsilon != 0.0f)
+  // Validation in the reference's order (numerics.cpp:30-49).  When the shapes,
+  // weight and epsilon are consistent the NaN/Inf scans of input and residual
+  // ride on the pipeline's staging copy (TW_HOST_CHECK_FINITE, same exception
+  // type and message); any structural problem takes the reference's serial
+  // order so the first exception thrown is the reference's.
+  auto structural_ok = [](const TokenMatrix& m) {
+    return m.num_tokens >= 0 && m.hidden >= 1 && m.values.size() == static_cast<size_t>(m.num_tokens * m.hidden);
+  };
+  const bool fast = structural_ok(input) && structural_ok(residual) && input.same_shape(residual) &&
+                    static_cast<std::int64_t>(params.weight.size()) == input.hidden &&
+                    (params.epsilon > 0.0f || params.epsilon == 0.0f);
+  if (!fast) {
+    input.validate();
+    residual.validate();
+    if (!input.same_shape(residual)) throw DimensionError("rmsnorm_residual: input and residual shapes differ");
+    if (static_cast<std::int64_t>(params.weight.size()) != input.hidden)
+      throw DimensionError("rmsnorm_residual: weight length must equal hidden size");
     throw NumericError("rmsnorm_residual: epsilon must be nonnegative");
+  }
   const std::int64_t T = input.num_tokens, H = input.hidden;
   NormResult result;
+  // The two fresh result matrices are value-initialised here, on the calling
+  // thread: a second thread would allocate from its own glibc arena, which
+  // measured 5x slower for 256 MiB blocks than the main heap.
   result.output = TokenMatrix::zeros(T, H);
   result.residual_out = TokenMatrix::zeros(T, H);
   if (T == 0) return result;
   device_count_or_throw();
   std::lock_guard<std::mutex> lock(g_mu);
-  // Host matrices in, host matrices out: the chunked H2D | K2 | D2H pipeline.
-  check(tw_rmsnorm_residual_host(input.values.data(), residual.values.data(), result.residual_out.values.data(),
-                                 result.output.values.data(), params.weight.data(), T, H, params.epsilon, TW_F32, 0,
-                                 nullptr),
-        "rmsnorm_residual");
-  check(tw_device_synchronize(0), "rmsnorm_residual");
+  // Host matrices in, host matrices out: pinned-ring staging by host threads
+  // around the chunked H2D | K2 | D2H pipeline.
+  const tw_status st = tw_rmsnorm_residual_host_sync(input.values.data(), residual.values.data(),
+                                                     result.residual_out.values.data(), result.output.values.data(),
+                                                     params.weight.data(), T, H, params.epsilon, TW_F32,
+                                                     TW_HOST_CHECK_FINITE);
+  if (st == TW_ERR_NUMERIC) throw NumericError("TokenMatrix contains NaN/Inf");
+  check(st, "rmsnorm_residual");
   return result;
 }
 
@@ -221,11 +238,45 @@ void upload_inputs(GroupContext& ctx, const RankGroup& group) {
   }
 }
 
+// RankGroups wider than a communicator (TW_MAX_RANKS): the rank-ascending
+// fp32 sum as a chain of K2 launches on device 0 -- K2's residual_out is
+// x + res in fp32, so acc <- in[r] + acc reproduces reduce_element's
+// ((0 + in[0]) + in[1]) + ... bit for bit (fp32 addition commutes; 0 + x = x).
+// Returns the device buffer holding the sum (scratch owned here).
+struct WideScratch {
+  DevBuf in, acc, tmp, out, weight;
+};
+WideScratch g_wide;  // guarded by g_mu
+
+void* chain_sum_on_device(const RankGroup& group) {
+  const std::int64_t T = group.num_tokens(), H = group.hidden();
+  const size_t nb = static_cast<size_t>(T * H) * sizeof(float);
+  WideScratch& w = g_wide;
+  for (DevBuf* b : {&w.in, &w.acc, &w.tmp, &w.out}) b->reserve(0, nb);
+  w.weight.reserve(0, static_cast<size_t>(H) * sizeof(float));
+  const std::vector<float> ones(static_cast<size_t>(H), 1.0f);
+  check(tw_memcpy(w.weight.ptr, ones.data(), ones.size() * sizeof(float), nullptr), "H2D weight");
+  check(tw_memcpy(w.acc.ptr, group.inputs[0].values.data(), nb, nullptr), "H2D input");  // 0 + in[0] == in[0]
+  for (int r = 1; r < group.world_size; ++r) {
+    check(tw_memcpy(w.in.ptr, group.inputs[r].values.data(), nb, nullptr), "H2D input");
+    check(tw_rmsnorm_residual(w.in.ptr, w.acc.ptr, w.tmp.ptr, w.out.ptr, static_cast<const float*>(w.weight.ptr), T,
+                              H, 0.0f, TW_F32, 0, nullptr),
+          "rank-order sum");
+    std::swap(w.acc.ptr, w.tmp.ptr);
+  }
+  check(tw_device_synchronize(0), "rank-order sum");
+  return w.acc.ptr;
+}
+
 TokenMatrix reduce_on_device(const RankGroup& group) {
   const std::int64_t T = group.num_tokens(), H = group.hidden();
   TokenMatrix out = TokenMatrix::zeros(T, H);
   if (T == 0) return out;
   const size_t nb = static_cast<size_t>(T * H) * sizeof(float);
+  if (group.world_size > TW_MAX_RANKS) {
+    check(tw_memcpy(out.values.data(), chain_sum_on_device(group), nb, nullptr), "D2H all_reduce");
+    return out;
+  }
   GroupContext& ctx = context_for(group.world_size, nb);
   upload_inputs(ctx, group);
   check(tw_allreduce_group(ctx.comm, T, H, 0, TW_F32, 8, nullptr), "all_reduce");
@@ -292,6 +343,30 @@ TokenMatrix fused_allreduce_rmsnorm(RankGroup& group, const NormParams& params, 
   const int W = group.world_size;
   const size_t nb = static_cast<size_t>(T * H) * sizeof(float);
   std::lock_guard<std::mutex> lock(g_mu);
+  if (W > TW_MAX_RANKS) {
+    // wider than a communicator: the chained rank-order sum, then one K2 over
+    // all T rows with the shards' residual rows (r' = v + res, the same fp32
+    // and double arithmetic as fused_rank_body, collectives.cpp:134-153)
+    void* sum = chain_sum_on_device(group);
+    WideScratch& w = g_wide;
+    std::vector<float> res(static_cast<size_t>(T * H));
+    for (int r = 0; r < W; ++r)
+      std::copy(group.residual_shards[r].values.begin(), group.residual_shards[r].values.end(),
+                res.begin() + shards.ranges[r].begin * H);
+    check(tw_memcpy(w.in.ptr, res.data(), nb, nullptr), "H2D residual");
+    check(tw_memcpy(w.weight.ptr, params.weight.data(), static_cast<size_t>(H) * sizeof(float), nullptr),
+          "H2D weight");
+    check(tw_rmsnorm_residual(sum, w.in.ptr, w.tmp.ptr, w.out.ptr, static_cast<const float*>(w.weight.ptr), T, H,
+                              params.epsilon, TW_F32, 0, nullptr),
+          "fused_allreduce_rmsnorm");
+    check(tw_device_synchronize(0), "fused_allreduce_rmsnorm");
+    check(tw_memcpy(output.values.data(), w.out.ptr, nb, nullptr), "D2H output");
+    check(tw_memcpy(res.data(), w.tmp.ptr, nb, nullptr), "D2H residual");
+    for (int r = 0; r < W; ++r)
+      std::copy(res.begin() + shards.ranges[r].begin * H, res.begin() + shards.ranges[r].end * H,
+                group.residual_shards[r].values.begin());
+    return output;
+  }
   GroupContext& ctx = context_for(W, nb);
   upload_inputs(ctx, group);
   std::vector<void*> res(W, nullptr);

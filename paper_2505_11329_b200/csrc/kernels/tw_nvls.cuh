@@ -33,18 +33,20 @@
 // the three multimem instructions need an NVSwitch.
 //
 // Memory ordering (PTX ISA memory model; see DESIGN.md §7 "NVLS ordering"):
-// INPUT is written by the producer through the unicast VA and read by peers'
-// ld_reduce through the multicast VA; OUTPUT/RESIDUAL are written through the
-// multicast VA and read by later kernels through the unicast VA.  Accesses to
-// one location through two virtual aliases need a proxy fence between them,
-// so thread 0 issues fence.proxy.alias where the alias changes: at entry
-// after its acquire (reads switch from the producer's unicast writes to the
-// multicast ld_reduce), at exit before its release (this CTA's multicast
-// stores, read through the unicast VA downstream).  It compiles to
-// MEMBAR.SC.GPU + MEMBAR.SC.SYS + CCTL.IVALL, so it is issued once per
-// barrier, not on both sides.  The arrival is a release at system scope
-// (multimem.red.release.sys), cumulative over the CTA's prior writes via
-// bar.sync; the wait is ld.acquire.sys on the local pad.
+// INPUT is written by the producer through the unicast VA (an earlier kernel)
+// and read by peers' ld_reduce through the multicast VA; OUTPUT/RESIDUAL are
+// written through the multicast VA and read by later kernels through the
+// unicast VA.  As in the paper's kernel (Listing 1:
+// sync_remote_blocks<Relaxed> at entry, <AcqRel> at exit):
+//  * entry: relaxed arrival + relaxed polls -- what it guards was written
+//    before this kernel started (complete at the kernel boundary);
+//  * exit: multimem.red.release.sys (MEMBAR.ALL.SYS + the reduction,
+//    cumulative over the CTA's stores via bar.sync), relaxed polls of the
+//    local pad, then one ld.acquire.sys of it (LDG.STRONG.SYS + CCTL.IVALL).
+// The cross-alias reads happen only in later kernels, so no fence.proxy.alias
+// is issued by default (TW_NVLS_ALIAS_FENCE=1 adds one before the exit
+// arrival: MEMBAR.SC.GPU + MEMBAR.SC.SYS + CCTL.IVALL, for A/B on hardware).
+// Each barrier thus costs one system-scope MEMBAR per CTA (the release).
 #pragma once
 
 #include <cstdint>
@@ -77,9 +79,16 @@ struct MmHw {
   static __device__ __forceinline__ void store_res(const RowParams& p, long long e, typename VT::Raw v) {
     VT::mm_store(p.mc_res, e, v);
   }
-  // One release-add on the multicast pad reaches counter b of every rank.
-  static __device__ __forceinline__ void arrive(const RowParams& p, int b) { mm_red_release_add(p.mc_pad + b, 1u); }
-  static __device__ __forceinline__ uint32_t poll(const uint32_t* pad) { return ld_acquire(pad); }
+  // One reduction on the multicast pad reaches counter b of every rank:
+  // release at exit, relaxed at entry (see nvls_barrier).
+  static __device__ __forceinline__ void arrive(const RowParams& p, int b, bool exit) {
+    if (exit)
+      mm_red_release_add(p.mc_pad + b, 1u);
+    else
+      mm_red_relaxed_add(p.mc_pad + b, 1u);
+  }
+  static __device__ __forceinline__ uint32_t poll(const uint32_t* pad) { return ld_relaxed_sys(pad); }
+  static __device__ __forceinline__ void acquire(const uint32_t* pad) { (void)ld_acquire(pad); }
 };
 
 struct MmSim {
@@ -116,28 +125,35 @@ struct MmSim {
     for (int q = 0; q < p.world; ++q) VT::store(p.peer_res[q], e, v);
   }
   // Co-located ranks share one GPU: device scope is the multicast's analogue.
-  static __device__ __forceinline__ void arrive(const RowParams& p, int b) {
-    fence_acq_rel_gpu();
+  static __device__ __forceinline__ void arrive(const RowParams& p, int b, bool exit) {
+    if (exit) fence_acq_rel_gpu();
     for (int q = 0; q < p.world; ++q) red_relaxed_add_gpu(p.peer_pad[q] + b, 1u);
   }
-  static __device__ __forceinline__ uint32_t poll(const uint32_t* pad) { return ld_acquire_gpu(pad); }
+  static __device__ __forceinline__ uint32_t poll(const uint32_t* pad) { return ld_relaxed_gpu(pad); }
+  static __device__ __forceinline__ void acquire(const uint32_t* pad) { (void)ld_acquire_gpu(pad); }
 };
 
 // phase 1 = entry, 2 = exit.  CTA b's g-th launch waits for its counter to
 // reach world * (2g + phase); the exit barrier advances the CTA's generation
 // (device-resident, so launches are graph-replayable without a host epoch).
+// Semantics as PAPER.md Listing 1 (sync_remote_blocks<Relaxed> at entry,
+// <AcqRel> at exit): the entry barrier publishes nothing this kernel wrote
+// (INPUT was written by earlier kernels, complete at the kernel boundary), so
+// it is a relaxed arrival + relaxed polls; the exit barrier releases this
+// CTA's multicast stores and acquires the peers'.
 template <class MM>
 __device__ __forceinline__ void nvls_barrier(const RowParams& p, const RankSlot& s, int phase) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const int b = blockIdx.x;
+    const bool exit = phase == 2;
     const uint32_t g = *reinterpret_cast<volatile uint32_t*>(s.gen + b);
     const uint32_t target = static_cast<uint32_t>(p.world) * (2u * g + static_cast<uint32_t>(phase));
     // exit: this CTA's multicast-VA stores (OUTPUT, RESIDUAL) are read
-    // through the unicast VA after the barrier -- proxy fence on the writer
-    // side, before the release-arrival.
-    if (phase == 2) fence_proxy_alias();
-    if (s.rank != p.drop_arrival_rank) MM::arrive(p, b);  // fault injection: a rank that never arrives
+    // through the unicast VA by later kernels; an optional proxy fence on the
+    // writer side (kAliasFence, off by default -- see tw_rownorm.cuh).
+    if (exit && (p.flags & kAliasFence)) fence_proxy_alias();
+    if (s.rank != p.drop_arrival_rank) MM::arrive(p, b, exit);  // fault injection: a rank that never arrives
     long long spins = 0;
     while (static_cast<int>(MM::poll(s.pad + b) - target) < 0) {
       if (++spins > p.spin_limit) {  // bounded: a rank was never launched / died
@@ -146,11 +162,10 @@ __device__ __forceinline__ void nvls_barrier(const RowParams& p, const RankSlot&
       }
       __nanosleep(32);
     }
-    // entry: INPUT, written through the unicast VA by each rank's producer,
-    // is about to be read through the multicast VA (ld_reduce) -- proxy
-    // fence on the reader side, after the acquire.
-    if (phase == 1) fence_proxy_alias();
-    if (phase == 2) s.gen[b] = g + 1u;
+    if (exit) {
+      MM::acquire(s.pad + b);  // one acquire load (no second MEMBAR.SYS)
+      s.gen[b] = g + 1u;
+    }
   }
   __syncthreads();
 }

@@ -85,6 +85,11 @@ struct RowParams {
 
 constexpr unsigned kGatherResidual = 0x1u;
 constexpr unsigned kDeviceScope = 0x100u;  // internal: every rank on this GPU (device-scope barriers)
+// internal (TW_NVLS_ALIAS_FENCE=1, A/B on an NVSwitch box): fence.proxy.alias
+// before the NVLS exit arrival.  Off by default, as in the paper's kernel
+// (Listing 1) and PyTorch's multimem AllReduce it builds on: the
+// multicast-VA stores are read through the unicast VA only by LATER kernels.
+constexpr unsigned kAliasFence = 0x200u;
 
 // ---- typed vector access -------------------------------------------------------
 // N elements of E per "vector": 8 x bf16 or 4 x f32 (16 B), or 1 element.
@@ -217,38 +222,58 @@ template <Xport X>
 // (only CTA b of this rank writes gen[b]; the next launch reads it after the
 // kernel boundary).  Every rank launches the same CTA count per call, so the
 // counters of CTA index b advance in lockstep across ranks.
+//
+// Memory semantics follow the paper's kernel (Listing 1:
+// sync_remote_blocks<Relaxed> at entry, <AcqRel> at exit):
+//  * entry publishes nothing this kernel wrote -- the INPUT rows were written
+//    by earlier kernels, complete at the kernel boundary -- so the arrival and
+//    the polls are relaxed: the barrier only says "every rank has started";
+//  * exit is a release (fence, then the arrival) of this CTA's stores and an
+//    acquire (relaxed polls, then one acquire load) of every peer's.
 __device__ __forceinline__ void rank_barrier(const RowParams& p, const RankSlot& s, int phase) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const int b = blockIdx.x;  // per-block-index counters: CTA b meets CTA b of every rank
     const uint32_t g = *reinterpret_cast<volatile uint32_t*>(s.gen + b);
     const uint32_t target = static_cast<uint32_t>(p.world) * (2u * g + static_cast<uint32_t>(phase));
-    // The CTA's prior writes are ordered before the arrival by bar.sync
-    // (cumulativity) + release semantics at system scope.
+    const bool exit = phase == 2;
+    const bool dev_scope = X != Xport::Nvls && (p.flags & kDeviceScope);
+    // The CTA's prior writes are ordered before the exit arrival by bar.sync
+    // (cumulativity) + the release fence.
     if (s.rank != p.drop_arrival_rank) {  // fault injection: a rank that never arrives
       if constexpr (X == Xport::Nvls) {
-        mm_red_release_add(p.mc_pad + b, 1u);  // one op reaches every rank's pad
-      } else {
-        if (p.flags & kDeviceScope) {
-          fence_acq_rel_gpu();
-          for (int q = 0; q < p.world; ++q) red_relaxed_add_gpu(p.peer_pad[q] + b, 1u);
+        if (exit) {
+          if (p.flags & kAliasFence) fence_proxy_alias();
+          mm_red_release_add(p.mc_pad + b, 1u);  // one op reaches every rank's pad
         } else {
-          fence_acq_rel_sys();
-          for (int q = 0; q < p.world; ++q) red_relaxed_add(p.peer_pad[q] + b, 1u);
+          mm_red_relaxed_add(p.mc_pad + b, 1u);
         }
+      } else if (dev_scope) {
+        if (exit) fence_acq_rel_gpu();
+        for (int q = 0; q < p.world; ++q) red_relaxed_add_gpu(p.peer_pad[q] + b, 1u);
+      } else {
+        if (exit) fence_acq_rel_sys();
+        for (int q = 0; q < p.world; ++q) red_relaxed_add(p.peer_pad[q] + b, 1u);
       }
     }
     long long spins = 0;
-    const bool dev_scope = X != Xport::Nvls && (p.flags & kDeviceScope);
-    while (static_cast<int>((dev_scope ? ld_acquire_gpu(s.pad + b) : ld_acquire(s.pad + b)) - target) < 0) {
+    while (static_cast<int>((dev_scope ? ld_relaxed_gpu(s.pad + b) : ld_relaxed_sys(s.pad + b)) - target) < 0) {
       if (++spins > p.spin_limit) {  // bounded: a rank was never launched / died
         atomicExch(p.err, 1);
         break;
       }
       __nanosleep(64);
     }
-    if constexpr (X == Xport::Nvls) fence_proxy_alias();
-    if (phase == 2) s.gen[b] = g + 1u;
+    if (exit) {
+      // acquire: one ld.acquire of the counter the relaxed polls saw reach the
+      // target (LDG.STRONG + CCTL.IVALL in SASS; a fence.acq_rel here would be
+      // a second MEMBAR.ALL.SYS, ~3 us at system scope)
+      if (dev_scope)
+        (void)ld_acquire_gpu(s.pad + b);
+      else
+        (void)ld_acquire(s.pad + b);
+      s.gen[b] = g + 1u;
+    }
   }
   __syncthreads();
 }

@@ -194,13 +194,24 @@ void gpu_cases() {
     exact = exact && sum.values[i] == e;
   }
   CHECK(exact);
+  RankGroup wide = random_group(13, 9, 12, 6);  // wider than a communicator
+  const TokenMatrix wsum = all_reduce(wide);
+  bool wexact = true;
+  for (std::int64_t i = 0; i < 9 * 12; ++i) {
+    float e = 0.0f;
+    for (const TokenMatrix& m : wide.inputs) e += m.values[i];
+    wexact = wexact && wsum.values[i] == e;
+  }
+  CHECK(wexact);
   for (std::int64_t tokens : {1, 7, 64, 129}) {
     RankGroup gg = random_group(8, tokens, 16, 1000 + tokens);
     const ShardMap shards = token_shard_map(tokens, 8);
     CHECK(all_reduce(gg).values == all_gather(reduce_scatter(gg, shards), shards).values);
   }
   // test_collectives.cpp:94-114 -- fused vs unfused composition
-  for (int world : {2, 4, 8}) {
+  // worlds above TW_MAX_RANKS take the drop-in's chained path (the reference
+  // accepts any N >= 2)
+  for (int world : {2, 4, 8, 12, 16}) {
     for (std::int64_t tokens : {1, 3, 17, 40}) {
       RankGroup group = random_group(world, tokens, 32, 77 * world + tokens);
       const ShardMap shards = token_shard_map(tokens, world);

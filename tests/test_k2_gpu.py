@@ -94,6 +94,48 @@ def test_k2_host_buffers_pipeline(cuda, orc, T, H, chunk, pinned):
     assert_bf16_close(out.float().numpy(), want_out)
 
 
+@pytest.mark.parametrize("dtype_name", ["float32", "bfloat16"])
+@pytest.mark.parametrize("T,H", [(1, 64), (37, 33), (513, 4096), (1100, 8192), (4096, 8192)])
+def test_k2_host_sync_pageable(cuda, orc, T, H, dtype_name):
+    """tw_rmsnorm_residual_host_sync on PAGEABLE numpy memory (pinned-ring
+    staging by host threads, chunks wrapping the ring several times) == the
+    oracle: fp32 residual bitwise / output <= 1e-5, bf16 as elsewhere."""
+    import ctypes
+    import paper_2505_11329_b200 as tw
+    from paper_2505_11329_b200 import _lib
+    inp, res, w = norm_inputs(3 * T + H, T, H)
+    bf = dtype_name == "bfloat16"
+    if bf:
+        inp, res = bf16_round(inp), bf16_round(res)
+    want_out, want_res = orc.rmsnorm_residual(inp, res, w)
+    if bf:
+        hi = (inp.view(np.uint32) >> 16).astype(np.uint16)
+        hr = (res.view(np.uint32) >> 16).astype(np.uint16)
+        ho, hro = np.empty_like(hi), np.empty_like(hi)
+    else:
+        hi, hr = np.ascontiguousarray(inp), np.ascontiguousarray(res)
+        ho, hro = np.empty_like(hi), np.empty_like(hi)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    tw.check(_lib.lib.tw_rmsnorm_residual_host_sync(p(hi), p(hr), p(hro), p(ho), p(w), T, H, 1e-5,
+                                                   tw.TW_BF16 if bf else tw.TW_F32, _lib.TW_HOST_CHECK_FINITE))
+    if bf:
+        up = lambda a: (a.astype(np.uint32) << 16).view(np.float32)  # noqa: E731
+        assert np.array_equal(up(hro), bf16_round(want_res))
+        assert_bf16_close(up(ho), want_out)
+    else:
+        assert np.array_equal(hro, want_res)
+        assert_abs_close(ho, want_out, 1e-5)
+    # a NaN anywhere (here: the residual's last chunk) -> NumericError
+    bad = hr.copy()
+    bad.reshape(-1)[-1] = 0x7FC0 if bf else np.float32("nan")
+    with pytest.raises(tw.NumericError):
+        tw.check(_lib.lib.tw_rmsnorm_residual_host_sync(p(hi), p(bad), p(hro), p(ho), p(w), T, H, 1e-5,
+                                                       tw.TW_BF16 if bf else tw.TW_F32, _lib.TW_HOST_CHECK_FINITE))
+    # without the flag the call does not scan
+    tw.check(_lib.lib.tw_rmsnorm_residual_host_sync(p(hi), p(hr), p(hro), p(ho), p(w), T, H, 1e-5,
+                                                   tw.TW_BF16 if bf else tw.TW_F32, 0))
+
+
 @pytest.mark.parametrize("engine,pipeline,groups", [("rows", "1", "1"), ("rows", "0", "1"), ("bulk", "0", "1"),
                                                     ("tma", "0", "1"), ("tma", "0", "2"), ("flat", "0", "1")])
 def test_k2_every_engine_matches_oracle(cuda, engine, pipeline, groups):

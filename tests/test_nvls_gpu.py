@@ -250,6 +250,35 @@ def test_nvls_sim_graph_replay(cuda, orc):
     comm.close()
 
 
+@pytest.mark.parametrize("env", [{"TW_NVLS_ALIAS_FENCE": "1"}, {"TW_FORCE_SYS_SCOPE": "1"},
+                                 {"TW_NVLS_ALIAS_FENCE": "1", "TW_FORCE_SYS_SCOPE": "1"}])
+def test_nvls_sim_barrier_variants(cuda, env):
+    """The barrier options read once per process (the optional proxy-alias
+    fence at exit; system-scope fences for co-located ranks): parity and
+    repeated launches in a fresh process with each set."""
+    code = textwrap.dedent("""
+        import sys
+        sys.path.insert(0, ".")
+        import numpy as np, torch
+        import paper_2505_11329_b200 as tw, oracle
+        from tests.test_nvls_gpu import make_comm, run_nvls, check_case, bf16_inputs
+        orc = oracle.Oracle()
+        for W, T, H in ((2, 33, 1024), (8, 128, 8192), (4, 7, 64)):
+            comm = make_comm(W, T * H * 2)
+            for it in range(3):
+                inputs, residual, weight = bf16_inputs(it + W, W, T, H)
+                ranges = tw.token_shard_map(T, W)
+                outs, res, g = run_nvls(comm, inputs, residual, weight, torch.bfloat16, ranges, gather=bool(it & 1),
+                                        sm_budget=4)
+                check_case(orc, inputs, residual, weight, ranges, torch.bfloat16, outs, res, g)
+            comm.close()
+        print("OK")
+    """)
+    p = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, **env))
+    assert p.returncode == 0 and "OK" in p.stdout, p.stdout[-2000:] + p.stderr[-3000:]
+
+
 def test_nvls_sim_barrier_timeout(cuda, monkeypatch):
     """A rank that never arrives: the bounded spin raises the timeout flag and
     tw_comm_check reports BarrierTimeout (no GPU hang); a fresh communicator

@@ -22,10 +22,13 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <malloc.h>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
+#include "tw/tw.h"
 #include "weavesim/collectives.hpp"
 #include "weavesim/numerics.hpp"
 
@@ -59,6 +62,13 @@ int main(int argc, char** argv) {
     return 2;
   }
   const std::string op = argv[1];
+  // Large blocks from the heap, kept across calls: repeated calls then reuse
+  // resident pages for the fresh result matrices, as the reference arm's
+  // 16 MB per-thread chunks do under glibc's adaptive mmap threshold
+  // (oracle/ref_capi.cpp sets the same).  Without it every 256 MiB result is
+  // a fresh mmap, page-faulted in (~100 ms per matrix on the GPU boxes' VMs).
+  mallopt(M_MMAP_MAX, 0);
+  mallopt(M_TRIM_THRESHOLD, 1 << 30);
   std::mt19937_64 rng(4321);
   NormParams p;
   if (op == "rmsnorm" && argc == 6) {
@@ -108,6 +118,43 @@ int main(int argc, char** argv) {
     }
     const std::int64_t nb = T * H * 4;
     emit("fused_allreduce_rmsnorm", ms, N * nb + nb + N * H * 4, 2 * nb);
+    return 0;
+  }
+  if (op == "phases" && argc == 5) {
+    // where the drop-in's time goes: the two fresh result matrices (zero-fill)
+    // vs the staged pipeline on already-allocated host memory
+    const std::int64_t T = std::atoll(argv[2]), H = std::atoll(argv[3]);
+    const int steps = std::atoi(argv[4]);
+    TokenMatrix in = TokenMatrix::zeros(T, H), res = TokenMatrix::zeros(T, H);
+    fill(in, rng);
+    fill(res, rng);
+    p.weight.assign(static_cast<size_t>(H), 1.0f);
+    TokenMatrix out = TokenMatrix::zeros(T, H), ro = TokenMatrix::zeros(T, H);
+    std::vector<double> alloc1, alloc2, pipe;
+    for (int i = 0; i < steps + 1; ++i) {
+      auto t0 = std::chrono::steady_clock::now();
+      { TokenMatrix a = TokenMatrix::zeros(T, H); }
+      auto t1 = std::chrono::steady_clock::now();
+      {
+        TokenMatrix a, b;
+        std::thread th([&] { b = TokenMatrix::zeros(T, H); });
+        a = TokenMatrix::zeros(T, H);
+        th.join();
+      }
+      auto t2 = std::chrono::steady_clock::now();
+      tw_status st = tw_rmsnorm_residual_host_sync(in.values.data(), res.values.data(), ro.values.data(),
+                                                   out.values.data(), p.weight.data(), T, H, 1e-5f, TW_F32,
+                                                   TW_HOST_CHECK_FINITE);
+      auto t3 = std::chrono::steady_clock::now();
+      if (st != TW_OK) return 1;
+      if (i == 0) continue;
+      alloc1.push_back(std::chrono::duration<double, std::milli>(t1 - t0).count());
+      alloc2.push_back(std::chrono::duration<double, std::milli>(t2 - t1).count());
+      pipe.push_back(std::chrono::duration<double, std::milli>(t3 - t2).count());
+    }
+    auto med = [](std::vector<double> v) { std::sort(v.begin(), v.end()); return v[v.size() / 2]; };
+    std::printf("{\"op\": \"phases\", \"zeros_one_ms\": %.3f, \"zeros_two_parallel_ms\": %.3f, "
+                "\"host_sync_pipeline_ms\": %.3f}\n", med(alloc1), med(alloc2), med(pipe));
     return 0;
   }
   std::fprintf(stderr, "bad arguments\n");
