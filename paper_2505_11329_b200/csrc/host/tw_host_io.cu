@@ -95,7 +95,7 @@ tw_status tw_rmsnorm_residual_host(const void* h_input, const void* h_residual, 
   if (!h_input || !h_residual || !h_residual_out || !h_output || !h_weight)
     return fail(TW_ERR_DIMENSION, "rmsnorm_residual_host: null buffer");
   const size_t row = static_cast<size_t>(H) * (dtype == TW_BF16 ? 2 : 4);
-  // ~8 MiB chunks (8-16 MiB measured best on B200 over PCIe Gen5, tools/e2e_probe.py)
+  // ~8 MiB chunks (8-16 MiB measured best on B200 over PCIe Gen5)
   if (chunk_rows <= 0) chunk_rows = std::max<int64_t>(1, static_cast<int64_t>((8u << 20) / row));
   chunk_rows = std::min<int64_t>(chunk_rows, T);
   int dev = 0;

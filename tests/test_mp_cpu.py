@@ -76,6 +76,18 @@ def test_nvlink_roofline_bytes():
     assert abs(algorithmic_nvlink_bytes(8192, 8192, 8, True) / 1e6 - 285.21) < 0.01
 
 
+def test_nvlink_counter_parse():
+    from tools.bench_tp import parse_nvlink_counters
+    text = """GPU 0: NVIDIA B200 (UUID: GPU-x)
+         Link 0: Data Tx: 1024 KiB
+         Link 0: Data Rx: 2048 KiB
+         Link 17: Data Tx: 1 KiB
+         Link 17: Data Rx: 3 KiB
+"""
+    assert parse_nvlink_counters(text) == (1025 * 1024, 2051 * 1024)
+    assert parse_nvlink_counters("NVLink not supported") is None
+
+
 def test_rendezvous_times_out_when_a_peer_never_arrives():
     """A rank that fails before the rendezvous must not hang the others: rank 0
     alone (and a rank without rank 0) give up after the bound."""

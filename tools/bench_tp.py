@@ -66,6 +66,11 @@ def nvlink_counters(device_index: int):
                              text=True, timeout=30).stdout
     except (OSError, subprocess.SubprocessError):
         return None
+    return parse_nvlink_counters(out)
+
+
+def parse_nvlink_counters(out: str):
+    """Sum the per-link "Data Tx/Rx: N KiB" lines of `nvidia-smi nvlink -gt d`."""
     tx = rx = 0
     seen = False
     for m in re.finditer(r"Link \d+: Data (Tx|Rx): (\d+) KiB", out):
@@ -281,6 +286,26 @@ def run_tp(args):
                 tw.rmsnorm_residual(nccl_buf, full_res, weight, residual_out=full_res, out=normed, stream=R.stream)
             base["nccl_allreduce_plus_k2_us"] = round(R.max_mean_us(R.timed(nccl_k2, 10, flush)), 2)
         extra["unfused_baselines"] = base
+        # the weave at TP = N: one Llama-3.3-70B layer at this
+        # TP's per-GPU GEMM shapes with K1 as the boundary op (tw_weave_create_tp)
+        try:
+            from paper_2505_11329_b200 import weave
+            r = weave.LayerRunner("llama-70b", tp=world, max_tokens=T, comm=R.h)
+            a, _, _, mode = weave.make_split_plan(T, threshold=r.threshold)
+            lay = {"T": T, "prefix": a if mode == 2 else None, "boundary_sms": budget}
+            for name, kw in (("unfused", {}), ("fuseonly", {}), ("nocomm", {}),
+                             ("tokenweave", {"prefix": a, "boundary_sms": budget})):
+                if name == "tokenweave" and mode != 2:
+                    continue
+                us_l = r.run(T, name, layers=4, **kw)
+                lay[name] = round(max_over_ranks(us_l, R.dist, R.red_device), 1)
+            lay["cublas_version"] = r.cublas_version
+            lay["note"] = ("per-layer device time, max over ranks, eager; GEMMs are cuBLAS load (not product); "
+                           "unfused = K3 AllReduce + add + RMSNorm on every rank")
+            r.close()
+            extra["weave_llama70b_layer_us"] = lay
+        except Exception as exc:  # noqa: BLE001 -- reported, never fatal
+            extra["weave_llama70b_layer_us"] = {"error": str(exc)[:200]}
 
     # ---- the reference CPU path at the same N (rank 0; others wait) ----
     cpu = None

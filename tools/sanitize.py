@@ -34,4 +34,20 @@ for W, H in ((2, 1024), (4, 1024), (8, 1024), (8, 8192), (2, 8192)):
     torch.cuda.synchronize()
     comm.check()
     comm.close()
+# K1 over NVLS (the north_star kernel) on simulated ranks: every pipeline
+# depth, G = 1/2, both dtypes, an uneven shard map
+for W, H, T in ((2, 8192, 29), (4, 1024, 13), (8, 8192, 21)):
+    comm = tw.Communicator(W, [0] * W, T * H * 4, tw.TW_TRANSPORT_NVLS_SIM)
+    for dt in (torch.bfloat16, torch.float32):
+        for q in range(W):
+            comm.buffer(q, 0, (T, H), dt).normal_()
+        ranges = tw.token_shard_map(T, W)
+        shards = [torch.randn(max(e - b, 1), H, device="cuda", dtype=dt) for b, e in ranges]
+        for depth in (1, 2, 3):
+            comm.fused_allreduce_rmsnorm(T, H, shards, [torch.ones(H, device="cuda")] * W, sm_budget=3,
+                                         gather_residual=depth == 2, dtype=dt, nvls_depth=depth)
+        comm.allreduce(T, H, dt, sm_budget=2)
+    torch.cuda.synchronize()
+    comm.check()
+    comm.close()
 print("sanitize workload done")
