@@ -320,6 +320,13 @@ tw_status tw_rmsnorm_residual_host_sync(const void* h_input, const void* h_resid
   e = cudaMemcpyAsync(c.weight, h_weight, H * sizeof(float), cudaMemcpyHostToDevice, c.h2d);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c.h2d);  // h_weight may be pageable and short-lived
   if (e != cudaSuccess) return cuda_fail(e, "host_sync: weight H2D");
+  // on any failure after work was enqueued: let the in-flight copies and
+  // kernels finish before returning, so no DMA still targets the pinned ring
+  // or the device slots when the next call reuses them
+  auto drain = [&](tw_status why) {
+    for (cudaStream_t q : {c.h2d, c.comp, c.d2h}) cudaStreamSynchronize(q);
+    return why;
+  };
   HostPool& pool = HostPool::get();
   const int parts = pool.size();
   const char* hin = static_cast<const char*>(h_input);
@@ -349,7 +356,7 @@ tw_status tw_rmsnorm_residual_host_sync(const void* h_input, const void* h_resid
   auto copy_out = [&](int64_t k) -> tw_status {
     const int s = static_cast<int>(k % kSlots);
     cudaError_t ee = cudaEventSynchronize(g.drained[s]);
-    if (ee != cudaSuccess) return cuda_fail(ee, "host_sync: D2H");
+    if (ee != cudaSuccess) return drain(cuda_fail(ee, "host_sync: D2H"));
     size_t off, nb;
     span(k, &off, &nb);
     pcopy(hout + off, static_cast<const char*>(g.h[s][2]), hro + off, static_cast<const char*>(g.h[s][3]), nb,
@@ -359,7 +366,7 @@ tw_status tw_rmsnorm_residual_host_sync(const void* h_input, const void* h_resid
   bool nonfinite = false;
   for (int64_t k = 0; k < K && !nonfinite; ++k) {
     const int s = static_cast<int>(k % kSlots);
-    if (k >= kSlots && (st = copy_out(k - kSlots)) != TW_OK) return st;  // also frees slot s's pinned in/out
+    if (k >= kSlots && (st = copy_out(k - kSlots)) != TW_OK) return drain(st);  // also frees slot s's pinned in/out
     size_t off, nb;
     span(k, &off, &nb);
     const int64_t n = static_cast<int64_t>(nb / row);
@@ -370,25 +377,22 @@ tw_status tw_rmsnorm_residual_host_sync(const void* h_input, const void* h_resid
     void** b = c.buf[s];
     if ((e = cudaMemcpyAsync(b[0], g.h[s][0], nb, cudaMemcpyHostToDevice, c.h2d)) != cudaSuccess ||
         (e = cudaMemcpyAsync(b[1], g.h[s][1], nb, cudaMemcpyHostToDevice, c.h2d)) != cudaSuccess)
-      return cuda_fail(e, "host_sync: H2D");
+      return drain(cuda_fail(e, "host_sync: H2D"));
     cudaEventRecord(c.loaded[s], c.h2d);
     cudaStreamWaitEvent(c.comp, c.loaded[s], 0);
     // (slot s's previous chunk, k - kSlots, was drained: copy_out synchronised on it)
     st = tw_rmsnorm_residual(b[0], b[1], b[3], b[2], static_cast<const float*>(c.weight), n, H, eps, dtype, 0, c.comp);
-    if (st != TW_OK) return st;
+    if (st != TW_OK) return drain(st);
     cudaEventRecord(c.computed[s], c.comp);
     cudaStreamWaitEvent(c.d2h, c.computed[s], 0);
     if ((e = cudaMemcpyAsync(g.h[s][2], b[2], nb, cudaMemcpyDeviceToHost, c.d2h)) != cudaSuccess ||
         (e = cudaMemcpyAsync(g.h[s][3], b[3], nb, cudaMemcpyDeviceToHost, c.d2h)) != cudaSuccess)
-      return cuda_fail(e, "host_sync: D2H");
+      return drain(cuda_fail(e, "host_sync: D2H"));
     cudaEventRecord(g.drained[s], c.d2h);
   }
-  if (nonfinite) {
-    for (cudaStream_t q : {c.h2d, c.comp, c.d2h}) cudaStreamSynchronize(q);
-    return fail(TW_ERR_NUMERIC, "TokenMatrix contains NaN/Inf");
-  }
+  if (nonfinite) return drain(fail(TW_ERR_NUMERIC, "TokenMatrix contains NaN/Inf"));
   for (int64_t k = std::max<int64_t>(0, K - kSlots); k < K; ++k)
-    if ((st = copy_out(k)) != TW_OK) return st;
+    if ((st = copy_out(k)) != TW_OK) return drain(st);
   cudaEventRecord(c.done, c.d2h);  // every chunk drained (copy_out synchronised on each)
   return TW_OK;
 }

@@ -122,6 +122,48 @@ def test_k1_gather_residual(cuda, orc, dtype_name, W, H):
         assert np.array_equal(gathered[r], full)
 
 
+@pytest.mark.parametrize("transport", ["peer", "nvls_sim"])
+def test_k1_colocated_per_rank_streams_are_joined(cuda, orc, transport):
+    """Co-located ranks launch as one grid on streams[0]; every other rank's
+    stream is joined before the launch and released after it: rank r's input
+    produced late on its own stream (behind a sleep kernel) is still what K1
+    reads, and work queued on stream r after the call sees K1's output."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    W, T, H = 4, 64, 1024
+    tr = tw.TW_TRANSPORT_PEER if transport == "peer" else tw.TW_TRANSPORT_NVLS_SIM
+    comm = tw.Communicator(W, [0] * W, T * H * 4, tr)
+    inputs, residual, weight = group_inputs(4242, W, T, H)
+    ranges = tw.token_shard_map(T, W)
+    inputs, residual, want_out, want_res = oracle_case(orc, inputs, residual, weight, ranges, True)
+    streams = [torch.cuda.Stream() for _ in range(W)]
+    shards = [torch.from_numpy(np.ascontiguousarray(residual[b:e])).cuda().bfloat16() for b, e in ranges]
+    wts = [torch.from_numpy(weight).cuda() for _ in range(W)]
+    host = [torch.from_numpy(inputs[r]).bfloat16().pin_memory() for r in range(W)]
+    for r in range(W):
+        comm.buffer(r, 0, (T, H), torch.bfloat16).fill_(float("nan"))
+    torch.cuda.synchronize()
+    for r in range(W):
+        with torch.cuda.stream(streams[r]):
+            torch.cuda._sleep(2_000_000)  # ~1 ms: the input lands well after the launch is enqueued
+            comm.buffer(r, 0, (T, H), torch.bfloat16).copy_(host[r], non_blocking=True)
+    comm.fused_allreduce_rmsnorm(T, H, shards, wts, shard_ranges=ranges, sm_budget=4, streams=streams)
+    copies = []
+    for r in range(W):
+        with torch.cuda.stream(streams[r]):
+            copies.append(comm.buffer(r, 1, (T, H), torch.bfloat16).float().clone())
+    torch.cuda.synchronize()
+    comm.check()
+    for r in range(W):
+        assert_bf16_close(copies[r].cpu().numpy(), want_out, what=f"rank {r} output read on its stream")
+        got = shards[r].float().cpu().numpy()
+        if transport == "peer":
+            assert np.array_equal(got, bf16_round(want_res[r])), f"rank {r} residual"
+        else:  # NVLS rounds the reduced sum once more (tests/test_nvls_gpu.py)
+            assert_bf16_close(got, want_res[r], what=f"rank {r} residual")
+    comm.close()
+
+
 def test_k1_uneven_and_empty_shards(cuda, orc):
     """Custom shard maps, including empty ranges (T < N)."""
     import torch

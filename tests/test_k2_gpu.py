@@ -94,6 +94,36 @@ def test_k2_host_buffers_pipeline(cuda, orc, T, H, chunk, pinned):
     assert_bf16_close(out.float().numpy(), want_out)
 
 
+def test_k2_host_pipeline_calls_on_different_streams(cuda, orc):
+    """Back-to-back host-buffer calls on two caller streams share one device
+    staging context: the second call's weight upload and staging slots wait
+    for the first call's kernels and copies, so both results are
+    right even though nothing orders the two caller streams."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    T, H = 3000, 8192
+    outs = []
+    cases = []
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for k in range(2):
+        inp, res, w = norm_inputs(900 + k, T, H)
+        inp, res = bf16_round(inp), bf16_round(res)
+        w = w * (1.0 + k)  # different weights: a race on the shared weight buffer shows
+        cases.append(orc.rmsnorm_residual(inp, res, w))
+        hi = torch.from_numpy(inp).bfloat16().pin_memory()
+        hr = torch.from_numpy(res).bfloat16().pin_memory()
+        ho = torch.empty(T, H, dtype=torch.bfloat16).pin_memory()
+        hro = torch.empty(T, H, dtype=torch.bfloat16).pin_memory()
+        outs.append((ho, hro, hi, hr))
+        tw.rmsnorm_residual_host(hi, hr, torch.from_numpy(w), residual_out=hro, out=ho, stream=streams[k])
+    torch.cuda.synchronize()
+    for k in range(2):
+        want_out, want_res = cases[k]
+        ho, hro = outs[k][0], outs[k][1]
+        assert np.array_equal(hro.float().numpy(), bf16_round(want_res)), k
+        assert_bf16_close(ho.float().numpy(), want_out, what=f"call {k}")
+
+
 @pytest.mark.parametrize("dtype_name", ["float32", "bfloat16"])
 @pytest.mark.parametrize("T,H", [(1, 64), (37, 33), (513, 4096), (1100, 8192), (4096, 8192)])
 def test_k2_host_sync_pageable(cuda, orc, T, H, dtype_name):
