@@ -417,6 +417,14 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
       // than groups (40 KB rows leave two stages: one group)
       if (q.groups * bp.tpr > kBulkMaxConsumers || stages <= q.groups) q.groups = 1;
       q.stages = stages;
+      // Loads in flight per SM: with a deep ring (>= 8 stages, rows <= 12.5 KB)
+      // two rows ahead of the oldest unarrived one, else the whole ring
+      // (tools/k2_policy_check.py A/B, profiles/k2_packed_ab_r02.txt: H = 6144,
+      // T = 8192 / 16384 65.5 -> 63.5 / 131 -> 124 us; neutral to +1 us at
+      // H = 8192's 6 stages; one row ahead loses 15-20 %).  TW_K2_LOOKAHEAD
+      // overrides (0 = the whole ring).
+      static const char* la_env = std::getenv("TW_K2_LOOKAHEAD");
+      q.lookahead = la_env ? std::max(0, std::atoi(la_env)) : (stages >= 8 ? 2 : 0);
       q.row_bytes = row_bytes;
       q.eps = eps;
       const long long ctas = static_cast<long long>(sms) * cps;

@@ -20,6 +20,18 @@
 
 namespace tw {
 
+// Per-CTA event timestamps for tools/probe/k2trace.cu (never defined in the product build).
+#ifdef TW_K2_TRACE
+__device__ unsigned long long k2_trace[1024 * 64];
+__device__ __forceinline__ void k2_tr(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (slot < 64) k2_trace[blockIdx.x * 64 + slot] = t;
+}
+#else
+__device__ __forceinline__ void k2_tr(int) {}
+#endif
+
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -83,6 +95,7 @@ struct BulkParams {
   int tpr;     // consumer threads per row group (multiple of 32)
   int groups;  // k2_tma_kernel: consumer row groups per CTA (1 or 2; groups * tpr <= 512)
   int stages;  // smem ring depth
+  int lookahead;  // k2_tma_kernel: rows of loads in flight ahead of the oldest unarrived one (0 = the ring)
   uint32_t row_bytes;
   float eps;
 };
@@ -228,6 +241,66 @@ __device__ __forceinline__ void sts_v4(void* p, uint4 v) {
 // after the bulk engine has finished READING it (bulk_wait_read<1> lags one
 // row so the store of row i overlaps the math of row i+1).  The SM's load/
 // store units only touch shared memory; HBM traffic is issued by TMA.
+// bf16 row math of k2_tma_kernel on packed lanes (sm_100a): r' with add.rn.bf16x2
+// (4 instructions per 8 elements instead of unpack + 8 fp32 adds + repack), the
+// sum of squares and out = (r' * inv) * w with f32x2 FFMA2/FMUL2.  Same values
+// as the scalar path (r' bitwise; ss summed as two interleaved fp32 partials).
+// Used with two row groups (the SM-budgeted and short-batch regime, where the
+// per-row latency bounds what one SM moves: 72.9 -> 80.5 GB/s per SM at an
+// 8-SM budget, H = 8192).  One group keeps the scalar path: with the packed
+// path a long batch (T = 16384, H = 8192) measured 178 vs 161 us
+// (profiles/k2_packed_ab_r02.txt).
+template <int VPT>
+__device__ __forceinline__ float k2_bf16_pass1(unsigned char* st, uint32_t row_bytes, int lt, int tpr, int V,
+                                               uint4 (&rr)[VPT]) {
+  float2 ss = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int c = lt + k * tpr;
+    if (c < V) {
+      const uint4 a = lds_v4(st + c * 16);
+      const uint4 b = lds_v4(st + row_bytes + c * 16);
+      uint4 r;
+      r.x = add_bf16x2(a.x, b.x);
+      r.y = add_bf16x2(a.y, b.y);
+      r.z = add_bf16x2(a.z, b.z);
+      r.w = add_bf16x2(a.w, b.w);
+      rr[k] = r;
+      sts_v4(st + row_bytes + c * 16, r);  // r' over the residual slot
+      float2 f = bf16x2_to_f32x2(r.x);
+      ss = __ffma2_rn(f, f, ss);
+      f = bf16x2_to_f32x2(r.y);
+      ss = __ffma2_rn(f, f, ss);
+      f = bf16x2_to_f32x2(r.z);
+      ss = __ffma2_rn(f, f, ss);
+      f = bf16x2_to_f32x2(r.w);
+      ss = __ffma2_rn(f, f, ss);
+    }
+  }
+  return ss.x + ss.y;
+}
+
+template <int VPT>
+__device__ __forceinline__ void k2_bf16_pass2(unsigned char* st, int lt, int tpr, int V, const uint4 (&rr)[VPT],
+                                              const float (&w)[VPT][8], float inv) {
+  const float2 inv2 = make_float2(inv, inv);
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int c = lt + k * tpr;
+    if (c < V) {
+      const uint32_t in[4] = {rr[k].x, rr[k].y, rr[k].z, rr[k].w};
+      uint32_t o[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float2 f = __fmul2_rn(bf16x2_to_f32x2(in[q]), inv2);
+        f = __fmul2_rn(f, make_float2(w[k][2 * q], w[k][2 * q + 1]));
+        o[q] = pack_bf16x2(f.x, f.y);
+      }
+      sts_v4(st + c * 16, make_uint4(o[0], o[1], o[2], o[3]));  // output over the input slot
+    }
+  }
+}
+
 template <class E, int VPT, int G>
 __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const __grid_constant__ BulkParams p) {
   // G (template: 1 or 2) consumer row groups: group g takes the CTA's rows i = g, g+G, ... (stage
@@ -255,22 +328,38 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
       mbar_init(&empty[s], 1);  // released by the storer of the row that used it
     }
     mbar_fence_init();
+    k2_tr(0);
   }
   __syncthreads();
   const long long nrows = p.T > blockIdx.x ? (p.T - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
   if (warp == 0) {
     if (lane == 0) {
+      // Lookahead L < S: row i is requested only once row i - L has ARRIVED,
+      // so at most L rows per SM are in flight.  When every SM requests its
+      // whole ring at once (short batches: T = 1024 is 7 rows per SM), the
+      // memory system interleaves all 148 x S rows and each SM's first row
+      // completes near the end of the read phase, leaving the consumers idle
+      // until then; a capped lookahead lets the first rows land early and the
+      // normalisation overlap the rest of the reads.  The stage of row i - L
+      // cannot have been refilled yet (this thread issues in order and L < S),
+      // so its full barrier has completed at most once: the parity wait is exact.
+      const int L = (p.lookahead > 0 && p.lookahead < S) ? p.lookahead : S;
       for (long long i = 0; i < nrows; ++i) {
         const int s = static_cast<int>(i % S);
         const uint32_t ph = static_cast<uint32_t>((i / S) & 1);
         if (i >= S) mbar_wait(&empty[s], ph ^ 1u);
+        if (L < S && i >= L) {
+          const long long j = i - L;
+          mbar_wait(&full[j % S], static_cast<uint32_t>((j / S) & 1));
+        }
         const long long row = blockIdx.x + i * gridDim.x;
         unsigned char* dst = ring + static_cast<size_t>(s) * 2 * p.row_bytes;
         mbar_arrive_expect_tx(&full[s], 2 * p.row_bytes);
         bulk_g2s(dst, static_cast<const unsigned char*>(p.in) + row * p.row_bytes, p.row_bytes, &full[s]);
         bulk_g2s(dst + p.row_bytes, static_cast<const unsigned char*>(p.res_in) + row * p.row_bytes, p.row_bytes,
                  &full[s]);
+        if (i < 8) k2_tr(1 + static_cast<int>(i));
       }
     }
     return;
@@ -286,30 +375,37 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     const int c = lt + k * tpr;
     if (c < p.V) load_weight<N>(p.weight, static_cast<long long>(c) * N, w[k]);
   }
+  if (lt == 0 && w[0][0] != 12345.0f) k2_tr(40 + grp);  // weights in registers
   for (long long i = grp; i < nrows; i += G) {
     const int s = static_cast<int>(i % S);
     const uint32_t ph = static_cast<uint32_t>((i / S) & 1);
     const long long row = blockIdx.x + i * gridDim.x;
     unsigned char* st = ring + static_cast<size_t>(s) * 2 * p.row_bytes;
     mbar_wait(&full[s], ph);
+    if (lt == 0 && i < 8) k2_tr(10 + static_cast<int>(i));
     typename VT::Raw rr[VPT];
     Acc ss = 0;
+    if constexpr (sizeof(E) == 2 && G == 2) {
+      ss = k2_bf16_pass1<VPT>(st, p.row_bytes, lt, tpr, p.V, rr);
+    } else {
 #pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      const int c = lt + k * tpr;
-      if (c < p.V) {
-        float x[N], r[N];
-        VT::unpack(lds_v4(st + c * 16), x);
-        VT::unpack(lds_v4(st + p.row_bytes + c * 16), r);
+      for (int k = 0; k < VPT; ++k) {
+        const int c = lt + k * tpr;
+        if (c < p.V) {
+          float x[N], r[N];
+          VT::unpack(lds_v4(st + c * 16), x);
+          VT::unpack(lds_v4(st + p.row_bytes + c * 16), r);
 #pragma unroll
-        for (int j = 0; j < N; ++j) r[j] = x[j] + r[j];
-        rr[k] = VT::pack(r);
-        VT::unpack(rr[k], r);
+          for (int j = 0; j < N; ++j) r[j] = x[j] + r[j];
+          rr[k] = VT::pack(r);
+          VT::unpack(rr[k], r);
 #pragma unroll
-        for (int j = 0; j < N; ++j) ss += static_cast<Acc>(r[j]) * static_cast<Acc>(r[j]);
-        sts_v4(st + p.row_bytes + c * 16, rr[k]);  // r' over the residual slot
+          for (int j = 0; j < N; ++j) ss += static_cast<Acc>(r[j]) * static_cast<Acc>(r[j]);
+          sts_v4(st + p.row_bytes + c * 16, rr[k]);  // r' over the residual slot
+        }
       }
     }
+    if (lt == 0 && i < 4 && ss != 12345.0f) k2_tr(44 + 4 * static_cast<int>(i));
     ss = warp_sum(ss);
     Acc total;
     Acc* pp = part + (grp * 2 + ((i / G) & 1)) * cwarps;
@@ -318,23 +414,31 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     total = 0;
     for (int q = 0; q < cwarps; ++q) total += pp[q];
     const float inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(p.H)) + p.eps);
+    if (lt == 0 && i < 4 && inv != 12345.0f) k2_tr(45 + 4 * static_cast<int>(i));
+    if constexpr (sizeof(E) == 2 && G == 2) {
+      k2_bf16_pass2<VPT>(st, lt, tpr, p.V, rr, w, inv);
+    } else {
 #pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      const int c = lt + k * tpr;
-      if (c < p.V) {
-        float o[N];
-        VT::unpack(rr[k], o);
+      for (int k = 0; k < VPT; ++k) {
+        const int c = lt + k * tpr;
+        if (c < p.V) {
+          float o[N];
+          VT::unpack(rr[k], o);
 #pragma unroll
-        for (int j = 0; j < N; ++j) o[j] = o[j] * inv * w[k][j];
-        sts_v4(st + c * 16, VT::pack(o));  // output over the input slot
+          for (int j = 0; j < N; ++j) o[j] = o[j] * inv * w[k][j];
+          sts_v4(st + c * 16, VT::pack(o));  // output over the input slot
+        }
       }
     }
+    if (lt == 0 && i < 4) k2_tr(46 + 4 * static_cast<int>(i));
     fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk engine
     named_bar_sync(G == 1 ? 1 : 1 + grp, tpr);
+    if (lt == 0 && i < 4) k2_tr(47 + 4 * static_cast<int>(i));
     if (storer) {
       bulk_s2g(static_cast<unsigned char*>(p.out) + row * p.row_bytes, st, p.row_bytes);
       bulk_s2g(static_cast<unsigned char*>(p.res_out) + row * p.row_bytes, st + p.row_bytes, p.row_bytes);
       bulk_commit();
+      if (i < 8) k2_tr(20 + static_cast<int>(i));
       // this storer's previous row (i - G) has finished reading its stage: free
       // it (a one-row lag, so the store overlaps the next row's math; freeing
       // each stage as soon as it is read stalls the group: -10-20 %,
@@ -346,7 +450,11 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     }
   }
   if (storer) {
-    bulk_wait_all();
+    // The stage must stay valid until the bulk engine has READ it; completion
+    // of the global writes is ordered by the kernel boundary (as CUTLASS's TMA
+    // store epilogues end on wait_group.read 0).
+    bulk_wait_read<0>();
+    k2_tr(30 + grp);
     if (nrows > grp) mbar_arrive(&empty[(grp + (nrows - 1 - grp) / G * G) % S]);
   }
 }

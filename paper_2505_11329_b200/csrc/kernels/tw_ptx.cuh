@@ -21,6 +21,16 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return r;
 }
 
+// r' = RNE(a + b) on two bf16 lanes: one rounding of the exact sum, the same
+// value as the fp32 add followed by an RNE pack (an fp32 sum of two bf16 values
+// is exact whenever the smaller one can affect the bf16 result).
+__device__ __forceinline__ uint32_t add_bf16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ float2 bf16x2_to_f32x2(uint32_t u) { return make_float2(bf16lo(u), bf16hi(u)); }
+
 __device__ __forceinline__ float bf16_to_f32(uint16_t b) { return __uint_as_float(uint32_t(b) << 16); }
 __device__ __forceinline__ uint16_t f32_to_bf16(float f) {
   return __bfloat16_as_ushort(__float2bfloat16_rn(f));

@@ -166,16 +166,21 @@ def test_k2_host_sync_pageable(cuda, orc, T, H, dtype_name):
                                                    tw.TW_BF16 if bf else tw.TW_F32, 0))
 
 
-@pytest.mark.parametrize("engine,pipeline,groups", [("rows", "1", "1"), ("rows", "0", "1"), ("bulk", "0", "1"),
-                                                    ("tma", "0", "1"), ("tma", "0", "2"), ("flat", "0", "1")])
-def test_k2_every_engine_matches_oracle(cuda, engine, pipeline, groups):
+@pytest.mark.parametrize("engine,pipeline,groups,lookahead",
+                         [("rows", "1", "1", "0"), ("rows", "0", "1", "0"), ("bulk", "0", "1", "0"),
+                          ("tma", "0", "1", "0"), ("tma", "0", "2", "0"), ("flat", "0", "1", "0"),
+                          ("tma", "0", "1", "1"), ("tma", "0", "2", "2"), ("tma", "0", "2", "3")])
+def test_k2_every_engine_matches_oracle(cuda, engine, pipeline, groups, lookahead):
     """Every K2 engine (and the software-pipelined row loop that the NVLS K1
-    path uses) against the oracle: the parity tests above re-run in a
-    subprocess with the engine forced (the selection is read once per process)."""
+    path uses), the TMA engine's one- and two-group row math (scalar / packed
+    bf16x2 + f32x2) and its load lookahead (rows in flight per SM) against the
+    oracle: the parity tests above re-run in a subprocess with the knobs forced
+    (they are read once per process)."""
     import os
     import subprocess
     import sys
-    env = dict(os.environ, TW_K2_ENGINE=engine, TW_ROWS_PIPELINE=pipeline, TW_K2_GROUPS=groups)
+    env = dict(os.environ, TW_K2_ENGINE=engine, TW_ROWS_PIPELINE=pipeline, TW_K2_GROUPS=groups,
+               TW_K2_LOOKAHEAD=lookahead)
     p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
                         "matches_oracle and not every_engine or in_place or full_size or host_buffers "
                         "or sm_budget or under_budget"],
