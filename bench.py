@@ -251,20 +251,22 @@ def k2_timed(T, H, steps, warmup, flush, seed=0):
     return [s.elapsed_time(e) for s, e in zip(starts, ends)], (x, r, w, out, rout)
 
 
-def k2_e2e(T, H, bufs, steps):
+def k2_e2e(T, H, bufs, steps, dtype=None):
     """The same op through the public C-ABI with HOST buffers:
     tw_rmsnorm_residual_host pipelines H2D | K2 | D2H in chunks.  Every step
     moves the whole input+residual host->device and output+residual_out
     device->host; the clock covers all of it (CUDA events on the caller's
-    stream, which the C-ABI joins back before returning)."""
+    stream, which the C-ABI joins back before returning).  dtype=torch.float32:
+    the reference's dtype (fp32 host matrices, fp32 K2)."""
     import torch
     import paper_2505_11329_b200 as tw
     x, r, w, _, _ = bufs
-    hx = x.cpu().pin_memory()
-    hr = r.cpu().pin_memory()
+    dt = dtype or torch.bfloat16
+    hx = x.to(dt).cpu().pin_memory()
+    hr = r.to(dt).cpu().pin_memory()
     hw = w.cpu()
-    ho = torch.empty(T, H, dtype=torch.bfloat16).pin_memory()
-    hro = torch.empty(T, H, dtype=torch.bfloat16).pin_memory()
+    ho = torch.empty(T, H, dtype=dt).pin_memory()
+    hro = torch.empty(T, H, dtype=dt).pin_memory()
     stream = torch.cuda.Stream()
     for _ in range(2):
         tw.rmsnorm_residual_host(hx, hr, hw, EPS, residual_out=hro, out=ho, stream=stream)
@@ -276,7 +278,7 @@ def k2_e2e(T, H, bufs, steps):
         ev[i + 1].record(stream)
     torch.cuda.synchronize()
     per = sorted(1e3 * ev[i].elapsed_time(ev[i + 1]) for i in range(steps))
-    nb = T * H * 2
+    nb = T * H * hx.element_size()
     # median step: one slow step (host memory contention on a shared box)
     # moved a 20-step mean by 60 % once; mean / min / max are reported beside it
     return {"value": round(per[len(per) // 2], 2), "unit": UNIT, "h2d_bytes_per_step": 2 * nb + 4 * H,
@@ -404,6 +406,7 @@ def run_ours_single(args):
         e2e = k2_e2e(T, H, bufs, max(3, min(args.steps, 20)))
         wall = time.perf_counter() - t0
     e2e_f32 = None if args.quick else dropin_f32_e2e(T, H, max(3, min(args.steps, 10)))  # same host binding
+    e2e_cabi_f32 = None if args.quick else k2_e2e(T, H, bufs, max(3, min(args.steps, 10)), torch.float32)
     os.sched_setaffinity(0, all_cpus)  # the CPU baseline below uses every host core
     avg_us = 1e3 * sum(times_ms) / len(times_ms)
     alg_bytes = 4 * T * H * 2 + 4 * H  # read input+residual, write residual_out+output (bf16) + fp32 weight
@@ -429,6 +432,11 @@ def run_ours_single(args):
     }
     if not args.quick:
         line["e2e_dropin_f32"] = dict(e2e_f32, host_binding=numa)
+        # the reference's dtype through the C-ABI over pinned buffers (no TokenMatrix vectors)
+        line["e2e_f32"] = dict(e2e_cabi_f32, dtype="f32", host_binding=numa,
+                               path="tw_rmsnorm_residual_host (C-ABI via ctypes), TW_F32: pinned fp32 host "
+                                    "input/residual -> chunked H2D | K2 (fp32) | D2H -> pinned fp32 output/residual_out; "
+                                    "same dtype and config as --impl reference")
         sweep = {}
         for t in (256, 1024, 2048, 4096, 8192, 16384):
             ts, _ = k2_timed(t, H, 20, 3, flush, seed=1)
@@ -462,12 +470,17 @@ def run_ours_single(args):
             line["weave_llama70b_tp8_shapes_us"] = {"error": str(exc)[:200]}
         threads = os.cpu_count() or 1
         cpu_ms = reference_rmsnorm_each_ms(T, H, threads, 4)[1:]
+        # the reference's API as one caller uses it: ONE rmsnorm_residual call on one thread
+        one_ms = reference_rmsnorm_each_ms(T, H, 1, 2)[1:]
         line["cpu_baseline"] = {
             "value": round(1e3 * statistics.median(cpu_ms), 1), "unit": UNIT, "cores": threads, "kind": "reference",
             "cpu": cpu_model(),
             "sample": f"full workload: weavesim::rmsnorm_residual (oracle/_ref, reference sources compiled "
                       f"unmodified) on {T}x{H} fp32, token rows chunked over {threads} threads (as "
-                      f"--impl reference), median of 3 after one warm-up; ms {[round(x, 1) for x in cpu_ms]}"}
+                      f"--impl reference), median of 3 after one warm-up; ms {[round(x, 1) for x in cpu_ms]}",
+            "single_call_1thread_us": round(1e3 * one_ms[0], 1),
+            "single_call_note": "one weavesim::rmsnorm_residual call on the whole matrix (the API is single-threaded; "
+                                "the drop-in's e2e_dropin_f32 is the same single call)"}
     line["wall_s"] = round(wall, 2)
     print(json.dumps(line), flush=True)
     return 0
