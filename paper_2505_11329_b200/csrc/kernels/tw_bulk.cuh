@@ -344,15 +344,7 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
       // normalisation overlap the rest of the reads.  The stage of row i - L
       // cannot have been refilled yet (this thread issues in order and L < S),
       // so its full barrier has completed at most once: the parity wait is exact.
-      const int L = (p.lookahead > 0 && p.lookahead < S) ? p.lookahead : S;
-      for (long long i = 0; i < nrows; ++i) {
-        const int s = static_cast<int>(i % S);
-        const uint32_t ph = static_cast<uint32_t>((i / S) & 1);
-        if (i >= S) mbar_wait(&empty[s], ph ^ 1u);
-        if (L < S && i >= L) {
-          const long long j = i - L;
-          mbar_wait(&full[j % S], static_cast<uint32_t>((j / S) & 1));
-        }
+      auto issue = [&](long long i, int s) {
         const long long row = blockIdx.x + i * gridDim.x;
         unsigned char* dst = ring + static_cast<size_t>(s) * 2 * p.row_bytes;
         mbar_arrive_expect_tx(&full[s], 2 * p.row_bytes);
@@ -360,6 +352,24 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
         bulk_g2s(dst + p.row_bytes, static_cast<const unsigned char*>(p.res_in) + row * p.row_bytes, p.row_bytes,
                  &full[s]);
         if (i < 8) k2_tr(1 + static_cast<int>(i));
+      };
+      const int L = p.lookahead;
+      if (L > 0 && L < S) {
+        for (long long i = 0; i < nrows; ++i) {
+          const int s = static_cast<int>(i % S);
+          if (i >= S) mbar_wait(&empty[s], static_cast<uint32_t>((i / S) & 1) ^ 1u);
+          if (i >= L) {
+            const long long j = i - L;
+            mbar_wait(&full[j % S], static_cast<uint32_t>((j / S) & 1));
+          }
+          issue(i, s);
+        }
+      } else {  // the whole ring in flight (kept as its own loop: the refill path is latency-critical)
+        for (long long i = 0; i < nrows; ++i) {
+          const int s = static_cast<int>(i % S);
+          if (i >= S) mbar_wait(&empty[s], static_cast<uint32_t>((i / S) & 1) ^ 1u);
+          issue(i, s);
+        }
       }
     }
     return;
