@@ -48,6 +48,47 @@ def test_k2_bf16_matches_oracle(cuda, orc, T, H):
     assert_bf16_close(out, want_out)
 
 
+def _bf16_rounding_edge_pairs(seed, T, H):
+    """bf16 (x, r) pairs that stress r' = RNE(x + r): every exponent gap 0..24
+    (the smaller operand's bits beyond, at and below bf16's half ulp), exact
+    ties onto even and odd mantissas in both signs, cancellation to +-0,
+    subnormals (down to 2^-133), and the normal/subnormal boundary."""
+    rng = np.random.default_rng(seed)
+    n = T * H
+    sign = lambda: np.where(rng.random(n) < 0.5, -1.0, 1.0)  # noqa: E731
+    mant = lambda: 1.0 + rng.integers(0, 128, n) / 128.0  # noqa: E731  (8 significant bits: exact in bf16)
+    e1 = rng.integers(-20, 12, n)
+    gap = rng.integers(0, 25, n)
+    x = sign() * mant() * np.exp2(e1)
+    r = sign() * mant() * np.exp2(e1 - gap)
+    kind = rng.integers(0, 6, n)
+    half_ulp = np.exp2(e1 - 8)  # x in [2^e1, 2^(e1+1)): bf16 ulp 2^(e1-7)
+    r = np.where(kind == 1, np.sign(r) * half_ulp, r)  # exact ties (either sign)
+    r = np.where(kind == 2, -x, r)  # cancellation
+    sub = np.exp2(rng.integers(-133, -120, n).astype(np.float64)) * mant()
+    x = np.where(kind == 3, sign() * sub, x)  # subnormal / boundary operands
+    r = np.where(kind == 3, sign() * np.exp2(rng.integers(-133, -118, n).astype(np.float64)), r)
+    r = np.where(kind == 4, sign() * half_ulp * 3, r)  # 1.5 ulp: rounds away from the tie
+    x32 = bf16_round(x.astype(np.float32)).reshape(T, H)
+    r32 = bf16_round(r.astype(np.float32)).reshape(T, H)
+    return x32, r32
+
+
+def test_k2_bf16_rounding_edges_matches_oracle(cuda, orc):
+    """r' bitwise = RNE(fp32 x + r) on crafted tie / gap / subnormal pairs (the
+    two-group engine forms r' with add.rn.bf16x2, the one-group engine with an
+    fp32 add and an RNE pack; the every-engine test re-runs this per engine)."""
+    import torch
+    for T in (64, 1500):  # two row groups, and many rows per CTA
+        x, r = _bf16_rounding_edge_pairs(91 + T, T, 8192)
+        w = np.random.default_rng(T).uniform(0.5, 1.5, 8192).astype(np.float32)
+        want_out, want_res = orc.rmsnorm_residual(x, r, w)
+        out, rout = run_k2(x, r, w, torch.bfloat16)
+        assert np.array_equal(rout.view(np.uint32), bf16_round(want_res).view(np.uint32)), \
+            "bf16 r' must be RNE(fp32 x + r), signed zeros included"
+        assert_bf16_close(out, want_out)
+
+
 def test_k2_in_place_residual(cuda, orc):
     import torch
     inp, res, w = norm_inputs(3, 40, 8192)
