@@ -210,7 +210,8 @@ def test_k2_host_sync_pageable(cuda, orc, T, H, dtype_name):
 @pytest.mark.parametrize("engine,pipeline,groups,lookahead",
                          [("rows", "1", "1", "0"), ("rows", "0", "1", "0"), ("bulk", "0", "1", "0"),
                           ("tma", "0", "1", "0"), ("tma", "0", "2", "0"), ("flat", "0", "1", "0"),
-                          ("tma", "0", "1", "1"), ("tma", "0", "2", "2"), ("tma", "0", "2", "3")])
+                          ("tma", "0", "1", "1"), ("tma", "0", "2", "2"), ("tma", "0", "2", "3"),
+                          ("tma", "0", "1", "0/256"), ("tma", "0", "1", "0/512")])
 def test_k2_every_engine_matches_oracle(cuda, engine, pipeline, groups, lookahead):
     """Every K2 engine (and the software-pipelined row loop that the NVLS K1
     path uses), the TMA engine's one- and two-group row math (scalar / packed
@@ -220,8 +221,11 @@ def test_k2_every_engine_matches_oracle(cuda, engine, pipeline, groups, lookahea
     import os
     import subprocess
     import sys
+    lookahead, _, tpr = lookahead.partition("/")  # "0/256": lookahead 0, 256 threads per row group
     env = dict(os.environ, TW_K2_ENGINE=engine, TW_ROWS_PIPELINE=pipeline, TW_K2_GROUPS=groups,
                TW_K2_LOOKAHEAD=lookahead)
+    if tpr:
+        env["TW_K2_TPR"] = tpr
     p = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", __file__, "-k",
                         "matches_oracle and not every_engine or in_place or full_size or host_buffers "
                         "or sm_budget or under_budget"],
