@@ -417,19 +417,9 @@ tw_status tw_rmsnorm_residual(const void* input, const void* residual, void* res
       // a group frees its stage one row late, so the ring needs more stages
       // than groups (40 KB rows leave two stages: one group)
       if (q.groups * bp.tpr > kBulkMaxConsumers || stages <= q.groups) q.groups = 1;
-      // One row group over 16 KB bf16 rows (H = 8192) at 48-80 rows per SM:
-      // 512 threads per row (two vectors each) instead of 256 -- the row's
-      // latency halves and T = 7168 / 8192 / 10240 run 74.5 / 84.2 / 103.0 us
-      // instead of 75.7 / 85.3 / 104.0 (bench-style mean of 50, same box);
-      // longer batches keep 256 (T = 12288 / 16384: 126 / 174 vs 123 / 165).
-      if (q.groups == 1 && !tpr_env && bf16 && row_bytes == 16 * 1024 && bp.tpr < 512 && T < 80LL * nsm) {
-        RowPlan wide;
-        if (plan_rows(H, nv, 512, &wide) && wide.tpr <= kBulkMaxConsumers) {
-          bp = wide;
-          q.V = bp.V;
-          q.tpr = bp.tpr;
-        }
-      }
+      // (512 threads per row for one group measured 1.4 % faster with a clean
+      // L2 but 2.5-9 % slower after a producer's dirty lines or back to back:
+      // not used, profiles/k2_packed_ab_r02.txt §5; TW_K2_TPR for A/B.)
       q.stages = stages;
       // Loads in flight per SM: with a deep ring (>= 8 stages, rows <= 12.5 KB)
       // two rows ahead of the oldest unarrived one, else the whole ring

@@ -4,7 +4,7 @@
 // issue, and the CTA's end, from %globaltimer (ns).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DTW_K2_TRACE \
 //      -I../../paper_2505_11329_b200/csrc -o k2trace k2trace.cu
-//   ./k2trace T [lookahead] [groups]
+//   ./k2trace T [lookahead] [groups] [threads per row group]
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -29,6 +29,7 @@ int main(int argc, char** argv) {
   const long long T = argc > 1 ? atoll(argv[1]) : 1024;
   const int la = argc > 2 ? atoi(argv[2]) : 0;
   const int G = argc > 3 ? atoi(argv[3]) : 2;
+  const int TPR = argc > 4 ? atoi(argv[4]) : 256;
   const long long H = 8192;
   const size_t bytes = size_t(T) * H * 2;
   void *x, *r, *ro, *o;
@@ -57,14 +58,15 @@ int main(int argc, char** argv) {
   p.T = T;
   p.H = H;
   p.V = int(H / 8);
-  p.tpr = 256;
+  p.tpr = TPR;
   p.groups = G;
   p.row_bytes = uint32_t(H * 2);
   p.stages = int(std::min<size_t>(8, (200 * 1024) / (2ull * p.row_bytes)));
   p.lookahead = la;
   p.eps = 1e-5f;
-  auto fn = G == 2 ? tw::k2_tma_kernel<uint16_t, 4, 2> : tw::k2_tma_kernel<uint16_t, 4, 1>;
-  const size_t smem = size_t(p.stages) * 2 * p.row_bytes + 2 * p.stages * 8 + 2 * G * 8 * 8;
+  auto fn = G == 2 ? (TPR == 512 ? tw::k2_tma_kernel<uint16_t, 2, 2> : tw::k2_tma_kernel<uint16_t, 4, 2>)
+                   : (TPR == 512 ? tw::k2_tma_kernel<uint16_t, 2, 1> : tw::k2_tma_kernel<uint16_t, 4, 1>);
+  const size_t smem = size_t(p.stages) * 2 * p.row_bytes + 2 * p.stages * 8 + 2 * G * (TPR / 32) * 8;
   cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   const int grid = int(std::min<long long>(T, nsm));
   cudaEvent_t s, e;
@@ -79,7 +81,7 @@ int main(int argc, char** argv) {
     fill_kernel<<<nsm * 4, 1024>>>(fl, flbytes / 16, it);
     read_kernel<<<nsm * 4, 1024>>>(fl, flbytes / 16, sink);
     cudaEventRecord(s);
-    fn<<<grid, G * 256 + 32, smem>>>(p);
+    fn<<<grid, G * TPR + 32, smem>>>(p);
     cudaEventRecord(e);
     cudaEventSynchronize(e);
     float ms = 0;
@@ -133,6 +135,17 @@ int main(int argc, char** argv) {
   }
   stat("end g0", 30);
   stat("end g1", 31);
+  {
+    std::vector<double> ends;
+    for (int b = 0; b < grid; ++b) {
+      double e = std::max(rel(b, 30), rel(b, 31));
+      if (e > 0) ends.push_back(e);
+    }
+    std::sort(ends.begin(), ends.end());
+    printf("  CTA end deciles:");
+    for (int q = 0; q <= 10; ++q) printf(" %.1f", ends[std::min(ends.size() - 1, ends.size() * q / 10)]);
+    printf("\n");
+  }
   printf("  CTA 0 :");
   for (int k : {0, 40, 1, 2, 3, 4, 5, 6, 7, 10, 11, 12, 13, 14, 15, 16, 20, 21, 22, 23, 24, 25, 26, 30, 31})
     printf(" %d:%.2f", k, rel(0, k));
