@@ -170,6 +170,12 @@ def reference_rmsnorm_each_ms(T, H, threads, iters):
     return oracle.RefLib().time_rmsnorm(T, H, threads, iters, each=True)
 
 
+def oracle_fused_ms(world, T, H, iters=3):
+    """The reference's fused_allreduce_rmsnorm(parallel=true), median ms (cpu_baseline leg only)."""
+    import oracle  # cpu_baseline / --impl reference legs only
+    return oracle.RefLib().time_fused(world, T, H, True, iters)
+
+
 def _reference_line(args, world, us, ms, sample, cores, workload):
     return {
         "impl": "reference", "metric": METRIC, "value": round(us, 1), "unit": UNIT, "n_gpus": world,
@@ -381,6 +387,25 @@ def dropin_f32_e2e(T, H, steps):
                     "--impl reference"}
 
 
+def dropin_fused_f32(world, T, H, steps):
+    """The reference's TP operator through the drop-in: weavesim::
+    fused_allreduce_rmsnorm(RankGroup&, NormParams, ShardMap, parallel=true)
+    with `world` fp32 ranks (tools/dropin_bench.cpp fused), the ranks
+    co-located on this one GPU (K1 over PEER) -- host matrices in and out."""
+    exe = os.path.join(ROOT, "build", "bench", "dropin_bench")
+    if not os.path.exists(exe):
+        return {"error": f"{exe} not built (make benchtools)"}
+    try:
+        p = subprocess.run([exe, "fused", str(world), str(T), str(H), "2", str(steps)], capture_output=True,
+                           text=True, timeout=600)
+        d = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1])
+    except Exception as exc:  # noqa: BLE001 -- reported, not fatal
+        return {"error": str(exc)[:200]}
+    return {"value": round(1e3 * d["median_ms"], 1), "unit": UNIT, "dtype": "f32", "world": world, "T": T, "H": H,
+            "steps": steps, "stat": "median wall time per call", "min": round(1e3 * d["min_ms"], 1),
+            "max": round(1e3 * d["max_ms"], 1)}
+
+
 def k2_traffic():
     """DRAM bytes per K2 launch from the newest committed ncu --set full capture."""
     for name in ("k2_ncu_r02.json", "k2_ncu_r01.json"):
@@ -432,6 +457,13 @@ def run_ours_single(args):
     }
     if not args.quick:
         line["e2e_dropin_f32"] = dict(e2e_f32, host_binding=numa)
+        # the TP path through the reference's own API: N fp32 ranks co-located on this GPU
+        line["dropin_fused_allreduce_rmsnorm_f32"] = {
+            f"tp{n}": dropin_fused_f32(n, 1024, H, max(3, min(args.steps, 5))) for n in (2, 8)}
+        line["dropin_fused_note"] = ("weavesim::fused_allreduce_rmsnorm(parallel=true) through libweavesim_b200.so, "
+                                     "1024 tok x H fp32, N ranks co-located on this one GPU (K1 over PEER, not "
+                                     "NVLink); the reference's own CPU path at the same N is cpu_baseline."
+                                     "fused_allreduce_rmsnorm_us")
         # the reference's dtype through the C-ABI over pinned buffers (no TokenMatrix vectors)
         line["e2e_f32"] = dict(e2e_cabi_f32, dtype="f32", host_binding=numa,
                                path="tw_rmsnorm_residual_host (C-ABI via ctypes), TW_F32: pinned fp32 host "
@@ -479,6 +511,8 @@ def run_ours_single(args):
                       f"unmodified) on {T}x{H} fp32, token rows chunked over {threads} threads (as "
                       f"--impl reference), median of 3 after one warm-up; ms {[round(x, 1) for x in cpu_ms]}",
             "single_call_1thread_us": round(1e3 * one_ms[0], 1),
+            "fused_allreduce_rmsnorm_us": {  # the reference's TP operator, parallel=true (one thread per rank)
+                f"tp{n}": round(1e3 * oracle_fused_ms(n, 1024, H), 1) for n in (2, 8)},
             "single_call_note": "one weavesim::rmsnorm_residual call on the whole matrix (the API is single-threaded; "
                                 "the drop-in's e2e_dropin_f32 is the same single call)"}
     line["wall_s"] = round(wall, 2)

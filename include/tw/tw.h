@@ -214,6 +214,19 @@ TW_API tw_status tw_device_free(int device, void* ptr);
 TW_API tw_status tw_memcpy(void* dst, const void* src, size_t bytes, void* stream);
 TW_API tw_status tw_device_synchronize(int device);
 
+/* Host (pageable or pinned) <-> device copies staged through the library's
+ * pinned ring by its pool of host threads: 8 MiB chunks, the host copy of one
+ * chunk overlapping the DMA of the others (a pageable cudaMemcpy is staged by
+ * the driver serially on the calling thread).  Ordered after the legacy
+ * default stream's prior work on the device that owns the device pointer;
+ * synchronous (return = copy complete).  The drop-in's RankGroup path.
+ * h2d: flags & TW_HOST_CHECK_FINITE scans the copied elements (dtype) for
+ * NaN/Inf on the way (TokenMatrix::validate's isfinite, numerics.cpp:25-27)
+ * and sets *nonfinite (the copy still completes). */
+TW_API tw_status tw_memcpy_h2d_staged(void* d_dst, const void* h_src, size_t bytes, tw_dtype dtype, unsigned flags,
+                                      int* nonfinite);
+TW_API tw_status tw_memcpy_d2h_staged(void* h_dst, const void* d_src, size_t bytes);
+
 /* Per-rank async error flag set by the in-kernel bounded barrier spin.
  * Returns TW_ERR_TIMEOUT (and clears the flag) if any rank timed out. */
 TW_API tw_status tw_comm_check(tw_comm_t comm);

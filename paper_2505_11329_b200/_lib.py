@@ -104,6 +104,8 @@ _SIGNATURES = [
     ("tw_device_alloc", c_int, [c_int, c_size_t, POINTER(c_void_p)]),
     ("tw_device_free", c_int, [c_int, c_void_p]),
     ("tw_memcpy", c_int, [c_void_p, c_void_p, c_size_t, c_void_p]),
+    ("tw_memcpy_h2d_staged", c_int, [c_void_p, c_void_p, c_size_t, c_int, c_uint, POINTER(c_int)]),
+    ("tw_memcpy_d2h_staged", c_int, [c_void_p, c_void_p, c_size_t]),
     ("tw_device_synchronize", c_int, [c_int]),
     ("tw_comm_check", c_int, [c_void_p]),
     ("tw_comm_create_mp", c_int, [c_int, c_int, c_int, c_size_t, c_char_p, c_int, POINTER(c_void_p)]),

@@ -65,6 +65,21 @@ int device_count_or_throw() {
   return n;
 }
 
+// Host matrices <-> device: staged through libtw's pinned ring by its host
+// thread pool (tw_memcpy_*_staged), not the driver's serial pageable staging.
+// scan = TokenMatrix::validate's NaN/Inf check riding on the copy; returns true
+// if a non-finite value was found.
+bool h2d(void* dst, const std::vector<float>& src, bool scan, const char* where) {
+  int nonfinite = 0;
+  check(tw_memcpy_h2d_staged(dst, src.data(), src.size() * sizeof(float), TW_F32, scan ? TW_HOST_CHECK_FINITE : 0u,
+                             &nonfinite),
+        where);
+  return nonfinite != 0;
+}
+void d2h(float* dst, const void* src, size_t bytes, const char* where) {
+  check(tw_memcpy_d2h_staged(dst, src, bytes), where);
+}
+
 // Cached communicator + per-rank scratch for the RankGroup API.
 struct GroupContext {
   tw_comm_t comm = nullptr;
@@ -229,13 +244,40 @@ void RankGroup::validate_residual(const ShardMap& shards) const {
 namespace {
 
 // Upload the group's inputs into the communicator's symmetric INPUT buffers.
-void upload_inputs(GroupContext& ctx, const RankGroup& group) {
-  const size_t nb = group.inputs[0].values.size() * sizeof(float);
+// scan: the inputs' NaN/Inf check rides on the copies (NumericError, the
+// reference's message, before anything user-visible is written).
+void upload_inputs(GroupContext& ctx, const RankGroup& group, bool scan = false) {
+  bool nonfinite = false;
   for (int r = 0; r < group.world_size; ++r) {
     void* dst = nullptr;
     check(tw_comm_buffer(ctx.comm, r, TW_BUF_INPUT, &dst), "comm_buffer");
-    check(tw_memcpy(dst, group.inputs[r].values.data(), nb, nullptr), "H2D inputs");
+    nonfinite |= h2d(dst, group.inputs[r].values, scan, "H2D inputs");
   }
+  if (nonfinite) throw NumericError("TokenMatrix contains NaN/Inf");
+}
+
+// The reference's validation of fused_allreduce_rmsnorm (collectives.cpp:41-69,
+// 157-163) WITHOUT its NaN/Inf scans: true when only a non-finite value could
+// still make it throw, so the scans can ride on the staging copies (same
+// exception, same message).  Anything else takes the reference's serial order.
+bool fused_structurally_ok(const RankGroup& g, const NormParams& params, const ShardMap& shards) {
+  auto ok = [](const TokenMatrix& m) {
+    return m.num_tokens >= 0 && m.hidden >= 1 && m.values.size() == static_cast<size_t>(m.num_tokens * m.hidden);
+  };
+  if (g.world_size < 2 || static_cast<int>(g.inputs.size()) != g.world_size) return false;
+  for (const TokenMatrix& m : g.inputs)
+    if (!ok(m) || !m.same_shape(g.inputs[0])) return false;
+  try {
+    shards.validate(g.num_tokens());
+  } catch (...) {
+    return false;
+  }
+  if (shards.world_size() != g.world_size || static_cast<int>(g.residual_shards.size()) != g.world_size) return false;
+  for (int r = 0; r < g.world_size; ++r) {
+    const TokenMatrix& m = g.residual_shards[r];
+    if (!ok(m) || m.num_tokens != shards.ranges[r].size() || m.hidden != g.hidden()) return false;
+  }
+  return static_cast<std::int64_t>(params.weight.size()) == g.hidden();
 }
 
 // RankGroups wider than a communicator (TW_MAX_RANKS): the rank-ascending
@@ -256,9 +298,9 @@ void* chain_sum_on_device(const RankGroup& group) {
   w.weight.reserve(0, static_cast<size_t>(H) * sizeof(float));
   const std::vector<float> ones(static_cast<size_t>(H), 1.0f);
   check(tw_memcpy(w.weight.ptr, ones.data(), ones.size() * sizeof(float), nullptr), "H2D weight");
-  check(tw_memcpy(w.acc.ptr, group.inputs[0].values.data(), nb, nullptr), "H2D input");  // 0 + in[0] == in[0]
+  h2d(w.acc.ptr, group.inputs[0].values, false, "H2D input");  // 0 + in[0] == in[0]
   for (int r = 1; r < group.world_size; ++r) {
-    check(tw_memcpy(w.in.ptr, group.inputs[r].values.data(), nb, nullptr), "H2D input");
+    h2d(w.in.ptr, group.inputs[r].values, false, "H2D input");
     check(tw_rmsnorm_residual(w.in.ptr, w.acc.ptr, w.tmp.ptr, w.out.ptr, static_cast<const float*>(w.weight.ptr), T,
                               H, 0.0f, TW_F32, 0, nullptr),
           "rank-order sum");
@@ -274,7 +316,7 @@ TokenMatrix reduce_on_device(const RankGroup& group) {
   if (T == 0) return out;
   const size_t nb = static_cast<size_t>(T * H) * sizeof(float);
   if (group.world_size > TW_MAX_RANKS) {
-    check(tw_memcpy(out.values.data(), chain_sum_on_device(group), nb, nullptr), "D2H all_reduce");
+    d2h(out.values.data(), chain_sum_on_device(group), nb, "D2H all_reduce");
     return out;
   }
   GroupContext& ctx = context_for(group.world_size, nb);
@@ -284,7 +326,7 @@ TokenMatrix reduce_on_device(const RankGroup& group) {
   check(tw_comm_check(ctx.comm), "all_reduce");
   void* src = nullptr;
   check(tw_comm_buffer(ctx.comm, 0, TW_BUF_OUTPUT, &src), "comm_buffer");
-  check(tw_memcpy(out.values.data(), src, nb, nullptr), "D2H all_reduce");
+  d2h(out.values.data(), src, nb, "D2H all_reduce");
   return out;
 }
 
@@ -333,10 +375,17 @@ TokenMatrix all_gather(const std::vector<TokenMatrix>& per_rank_shards, const Sh
 
 TokenMatrix fused_allreduce_rmsnorm(RankGroup& group, const NormParams& params, const ShardMap& shards,
                                     bool /*parallel*/) {
-  group.validate();
-  group.validate_residual(shards);
-  if (static_cast<std::int64_t>(params.weight.size()) != group.hidden())
-    throw DimensionError("fused_allreduce_rmsnorm: weight length must equal hidden size");
+  // The reference's checks in its order; when the structure is sound the
+  // NaN/Inf scans of the inputs and shards ride on the staging copies below.
+  // (no GPU visible: the serial order, so a NaN is still a NumericError, not a DeviceError)
+  const bool fast =
+      fused_structurally_ok(group, params, shards) && group.world_size <= TW_MAX_RANKS && tw_device_count() > 0;
+  if (!fast) {
+    group.validate();
+    group.validate_residual(shards);
+    if (static_cast<std::int64_t>(params.weight.size()) != group.hidden())
+      throw DimensionError("fused_allreduce_rmsnorm: weight length must equal hidden size");
+  }
   const std::int64_t T = group.num_tokens(), H = group.hidden();
   TokenMatrix output = TokenMatrix::zeros(T, H);
   if (T == 0) return output;
@@ -353,22 +402,22 @@ TokenMatrix fused_allreduce_rmsnorm(RankGroup& group, const NormParams& params, 
     for (int r = 0; r < W; ++r)
       std::copy(group.residual_shards[r].values.begin(), group.residual_shards[r].values.end(),
                 res.begin() + shards.ranges[r].begin * H);
-    check(tw_memcpy(w.in.ptr, res.data(), nb, nullptr), "H2D residual");
+    h2d(w.in.ptr, res, false, "H2D residual");
     check(tw_memcpy(w.weight.ptr, params.weight.data(), static_cast<size_t>(H) * sizeof(float), nullptr),
           "H2D weight");
     check(tw_rmsnorm_residual(sum, w.in.ptr, w.tmp.ptr, w.out.ptr, static_cast<const float*>(w.weight.ptr), T, H,
                               params.epsilon, TW_F32, 0, nullptr),
           "fused_allreduce_rmsnorm");
     check(tw_device_synchronize(0), "fused_allreduce_rmsnorm");
-    check(tw_memcpy(output.values.data(), w.out.ptr, nb, nullptr), "D2H output");
-    check(tw_memcpy(res.data(), w.tmp.ptr, nb, nullptr), "D2H residual");
+    d2h(output.values.data(), w.out.ptr, nb, "D2H output");
+    d2h(res.data(), w.tmp.ptr, nb, "D2H residual");
     for (int r = 0; r < W; ++r)
       std::copy(res.begin() + shards.ranges[r].begin * H, res.begin() + shards.ranges[r].end * H,
                 group.residual_shards[r].values.begin());
     return output;
   }
   GroupContext& ctx = context_for(W, nb);
-  upload_inputs(ctx, group);
+  upload_inputs(ctx, group, fast);
   std::vector<void*> res(W, nullptr);
   std::vector<const float*> wts(W, nullptr);
   std::vector<std::int64_t> flat;
@@ -376,7 +425,8 @@ TokenMatrix fused_allreduce_rmsnorm(RankGroup& group, const NormParams& params, 
     const size_t rb = group.residual_shards[r].values.size() * sizeof(float);
     ctx.residual[r].reserve(ctx.devices[r], rb);
     ctx.weight[r].reserve(ctx.devices[r], H * sizeof(float));
-    check(tw_memcpy(ctx.residual[r].ptr, group.residual_shards[r].values.data(), rb, nullptr), "H2D residual");
+    if (h2d(ctx.residual[r].ptr, group.residual_shards[r].values, fast, "H2D residual"))
+      throw NumericError("TokenMatrix contains NaN/Inf");
     check(tw_memcpy(ctx.weight[r].ptr, params.weight.data(), H * sizeof(float), nullptr), "H2D weight");
     res[r] = rb ? ctx.residual[r].ptr : nullptr;
     wts[r] = static_cast<const float*>(ctx.weight[r].ptr);
@@ -390,10 +440,10 @@ TokenMatrix fused_allreduce_rmsnorm(RankGroup& group, const NormParams& params, 
   check(tw_comm_check(ctx.comm), "fused_allreduce_rmsnorm");
   void* src = nullptr;
   check(tw_comm_buffer(ctx.comm, 0, TW_BUF_OUTPUT, &src), "comm_buffer");
-  check(tw_memcpy(output.values.data(), src, nb, nullptr), "D2H output");
+  d2h(output.values.data(), src, nb, "D2H output");
   for (int r = 0; r < W; ++r) {
     const size_t rb = group.residual_shards[r].values.size() * sizeof(float);
-    check(tw_memcpy(group.residual_shards[r].values.data(), ctx.residual[r].ptr, rb, nullptr), "D2H residual");
+    d2h(group.residual_shards[r].values.data(), ctx.residual[r].ptr, rb, "D2H residual");
   }
   return output;
 }

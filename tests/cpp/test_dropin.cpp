@@ -235,6 +235,33 @@ void gpu_cases() {
   const TokenMatrix b = fused_allreduce_rmsnorm(par, unit_norm(24), s53, true);
   CHECK(a.values == b.values);
   for (int r = 0; r < 8; ++r) CHECK(seq.residual_shards[r].values == par.residual_shards[r].values);
+  // NaN/Inf anywhere in the group -> NumericError with the residual shards
+  // untouched (the drop-in scans while staging the copies; the reference
+  // validates first), and a structural error still wins over a NaN wherever
+  // the reference checks structure first
+  for (int world : {2, 8}) {
+    RankGroup clean = random_group(world, 40, 64, 5 + world);
+    const ShardMap sh = token_shard_map(40, world);
+    RankGroup nan_in = clean;
+    nan_in.inputs[world - 1].values[64 * 17 + 3] = std::nanf("");
+    CHECK_THROWS_AS(fused_allreduce_rmsnorm(nan_in, unit_norm(64), sh), NumericError);
+    CHECK(nan_in.residual_shards[0].values == clean.residual_shards[0].values);
+    RankGroup inf_res = clean;
+    inf_res.residual_shards[1].values.back() = -INFINITY;
+    CHECK_THROWS_AS(fused_allreduce_rmsnorm(inf_res, unit_norm(64), sh), NumericError);
+    CHECK(inf_res.residual_shards[0].values == clean.residual_shards[0].values);
+    CHECK_THROWS_AS(fused_allreduce_rmsnorm(nan_in, unit_norm(63), sh), NumericError);  // validate() precedes the weight check
+    RankGroup nan_bad_shard = nan_in;
+    nan_bad_shard.residual_shards[0] = TokenMatrix::zeros(3, 64);
+    CHECK_THROWS_AS(fused_allreduce_rmsnorm(nan_bad_shard, unit_norm(64), sh), NumericError);  // inputs first
+    RankGroup bad_shard = clean;
+    bad_shard.residual_shards[0] = TokenMatrix::zeros(3, 64);
+    CHECK_THROWS_AS(fused_allreduce_rmsnorm(bad_shard, unit_norm(64), sh), DimensionError);
+    // and the same group without the NaN still computes (the cached state is intact)
+    RankGroup again = clean;
+    const TokenMatrix out = fused_allreduce_rmsnorm(again, unit_norm(64), sh);
+    CHECK(out.values.size() == static_cast<size_t>(40 * 64));
+  }
 }
 
 // acceptance.cpp:37-86 -- the fused op vs the unfused chain over the
