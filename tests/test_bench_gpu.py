@@ -44,7 +44,7 @@ def test_bench_single_gpu_line():
     # the reference's own C++ API and dtype through the drop-in (same config as --impl reference)
     f32 = d["e2e_dropin_f32"]
     assert f32["dtype"] == "f32" and f32["value"] > 0 and f32["h2d_bytes_per_step"] > 0, f32
-    assert d["kernel_us"]["back_to_back_no_flush"] > 0
+    assert d["kernel_us"]["back_to_back_no_flush"] > 0 and d["kernel_us"]["after_dirty_l2"] > 0
     assert set(d["weave_llama70b_tp8_shapes_us"]["tokenweave_by_boundary_sms"]) == {"16", "32", "64"}
 
 
