@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(1024) add_stream(const uint4* __restrict__ x, 
 
 int main() {
   const size_t H = 8192;
-  const size_t Tmax = 4096;
+  const size_t Tmax = 16384;
   const size_t bytes = Tmax * H * 2;
   uint4 *x, *r, *ro, *o, *fl;
   uint32_t* sink;
@@ -102,7 +102,7 @@ int main() {
   };
   printf("empty1 %.2f us\n", timeit([&] { empty_kernel<<<1, 32>>>(); }));
   printf("emptyfull %.2f us\n", timeit([&] { empty_kernel<<<nsm, 544, 197 * 1024>>>(); }));
-  for (size_t T : {256, 1024, 2048, 4096}) {
+  for (size_t T : {256, 1024, 2048, 4096, 8192, 16384}) {
     const size_t n = T * H * 2 / 16;
     const double alg = 4.0 * T * H * 2;
     float t1 = timeit([&] { add_stream<1><<<nsm * 2, 1024>>>(x, r, ro, o, n); });
