@@ -310,7 +310,9 @@ void* chain_sum_on_device(const RankGroup& group) {
   return w.acc.ptr;
 }
 
-TokenMatrix reduce_on_device(const RankGroup& group) {
+// scan: the inputs' NaN/Inf check of RankGroup::validate rides on the upload
+// (the caller has checked everything else, in the reference's order).
+TokenMatrix reduce_on_device(const RankGroup& group, bool scan = false) {
   const std::int64_t T = group.num_tokens(), H = group.hidden();
   TokenMatrix out = TokenMatrix::zeros(T, H);
   if (T == 0) return out;
@@ -320,7 +322,7 @@ TokenMatrix reduce_on_device(const RankGroup& group) {
     return out;
   }
   GroupContext& ctx = context_for(group.world_size, nb);
-  upload_inputs(ctx, group);
+  upload_inputs(ctx, group, scan);
   check(tw_allreduce_group(ctx.comm, T, H, 0, TW_F32, 8, nullptr), "all_reduce");
   for (int d : ctx.devices) check(tw_device_synchronize(d), "all_reduce");
   check(tw_comm_check(ctx.comm), "all_reduce");
@@ -330,21 +332,47 @@ TokenMatrix reduce_on_device(const RankGroup& group) {
   return out;
 }
 
+// RankGroup::validate without its NaN/Inf scans (collectives.cpp:41-50): when
+// true, the scans ride on the staged upload (same exception and message).
+bool inputs_structurally_ok(const RankGroup& g) {
+  if (g.world_size < 2 || static_cast<int>(g.inputs.size()) != g.world_size || g.world_size > TW_MAX_RANKS ||
+      tw_device_count() < 1)
+    return false;
+  for (const TokenMatrix& m : g.inputs)
+    if (m.num_tokens < 0 || m.hidden < 1 || m.values.size() != static_cast<size_t>(m.num_tokens * m.hidden) ||
+        !m.same_shape(g.inputs[0]))
+      return false;
+  return true;
+}
+
 }  // namespace
 
 TokenMatrix all_reduce(const RankGroup& group) {
-  group.validate();
+  const bool fast = inputs_structurally_ok(group);
+  if (!fast) group.validate();
   std::lock_guard<std::mutex> lock(g_mu);
-  return reduce_on_device(group);
+  return reduce_on_device(group, fast);
 }
 
 std::vector<TokenMatrix> reduce_scatter(const RankGroup& group, const ShardMap& shards) {
-  group.validate();
-  shards.validate(group.num_tokens());
+  // the reference validates the group (NaN/Inf included) BEFORE the shard map:
+  // the scan may ride on the upload only when the shard map is valid too
+  bool fast = inputs_structurally_ok(group);
+  if (fast) {
+    try {
+      shards.validate(group.num_tokens());
+    } catch (...) {
+      fast = false;
+    }
+  }
+  if (!fast) {
+    group.validate();
+    shards.validate(group.num_tokens());
+  }
   TokenMatrix sum;
   {
     std::lock_guard<std::mutex> lock(g_mu);
-    sum = reduce_on_device(group);
+    sum = reduce_on_device(group, fast);
   }
   const std::int64_t H = group.hidden();
   std::vector<TokenMatrix> out;

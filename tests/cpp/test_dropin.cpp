@@ -257,6 +257,12 @@ void gpu_cases() {
     RankGroup bad_shard = clean;
     bad_shard.residual_shards[0] = TokenMatrix::zeros(3, 64);
     CHECK_THROWS_AS(fused_allreduce_rmsnorm(bad_shard, unit_norm(64), sh), DimensionError);
+    CHECK_THROWS_AS(all_reduce(nan_in), NumericError);
+    CHECK_THROWS_AS(reduce_scatter(nan_in, sh), NumericError);
+    ShardMap bad_map = sh;
+    bad_map.ranges[0].end += 1;
+    CHECK_THROWS_AS(reduce_scatter(nan_in, bad_map), NumericError);  // the group before the shard map
+    CHECK_THROWS_AS(reduce_scatter(clean, bad_map), ContractError);
     // and the same group without the NaN still computes (the cached state is intact)
     RankGroup again = clean;
     const TokenMatrix out = fused_allreduce_rmsnorm(again, unit_norm(64), sh);
