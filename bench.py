@@ -65,6 +65,17 @@ class L2Flush:
         self.sink.copy_(self.buf.view(-1).view(__import__("torch").float32).sum().reshape(1))
 
 
+def smi_id(local_index: int) -> str:
+    """nvidia-smi's id for CUDA device `local_index`: its UUID (CUDA_VISIBLE_DEVICES
+    may renumber devices, nvidia-smi does not), else the index."""
+    try:
+        import torch
+        u = str(torch.cuda.get_device_properties(local_index).uuid)
+        return u if u.startswith("GPU-") else f"GPU-{u}"
+    except Exception:
+        return str(local_index)
+
+
 class ClockSampler:
     """nvidia-smi SM clocks + throttle reasons sampled during the timed region."""
 
@@ -74,7 +85,7 @@ class ClockSampler:
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int = 0):
-        self.index = index
+        self.index = smi_id(index)
         self.samples = []
         self._stop = threading.Event()
         self._t = None

@@ -62,7 +62,8 @@ def nvlink_counters(device_index: int):
     """(tx_bytes, rx_bytes) summed over the GPU's NVLink links from the
     driver's data counters (`nvidia-smi nvlink -gt d`), or None."""
     try:
-        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(device_index)], capture_output=True,
+        from bench import smi_id
+        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", smi_id(device_index)], capture_output=True,
                              text=True, timeout=30).stdout
     except (OSError, subprocess.SubprocessError):
         return None
