@@ -11,14 +11,16 @@ import pytest
 from tests.conftest import ROOT
 
 PROBE = r"""
-import json, sys
+import json, os, sys
+root = os.path.realpath(os.getcwd())
 sys.argv = ["bench.py", "--impl", "reference", "--steps", "2", "--warmup", "1", "--tokens", "256",
             "--hidden", "512", "--gpus", GPUS]
 sys.path.insert(0, ".")
 import bench
 rc = bench.main()
 maps = open("/proc/self/maps").read()
-libs = sorted({ln.split()[-1] for ln in maps.splitlines() if ln.endswith(".so") and "/repo" in ln or "libtw" in ln})
+libs = sorted({ln.split()[-1] for ln in maps.splitlines()
+               if ln.endswith(".so") and (root in os.path.realpath(ln.split()[-1]) or "libtw" in ln)})
 print(json.dumps({"rc": rc, "libs": libs, "pkg": [m for m in sys.modules if m.startswith("paper_2505")]}))
 """
 
