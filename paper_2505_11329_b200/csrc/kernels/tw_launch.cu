@@ -68,23 +68,52 @@ __global__ void __launch_bounds__(kBlock, 1) allreduce_kernel(const __grid_const
   rank_barrier<X>(p, s, 1);
   const long long n = (s.end - s.begin) * p.V;  // vectors in the shard
   const long long base = (p.row_offset + s.begin) * p.H;
-  for (long long v = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; v < n;
-       v += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long e = base + v * N;
-    if constexpr (X == Xport::Nvls) {
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  if constexpr (X == Xport::Nvls) {
+    for (long long v = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride) {
+      const long long e = base + v * N;
       VT::mm_store(p.mc_out, e, VT::mm_reduce(p.mc_in, e));
-    } else {
-      float acc[N];
+    }
+  } else {
+    // U vectors per thread per pass and the peers' loads issued four at a
+    // time before they are summed (a load-then-add loop over the ranks kept
+    // ~one load in flight per thread: the baseline ran at ~50 % of HBM).  The
+    // sum stays rank-ascending fp32 from 0 (reduce_element,
+    // collectives.cpp:74-78), so results are unchanged bit for bit.
+    constexpr int U = 2;
+    for (long long v0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; v0 < n; v0 += U * stride) {
+      float acc[U][N];
 #pragma unroll
-      for (int i = 0; i < N; ++i) acc[i] = 0.0f;
-      for (int q = 0; q < p.world; ++q) {
-        float f[N];
-        VT::unpack(VT::load(p.peer_in[q], e), f);
+      for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int i = 0; i < N; ++i) acc[i] += f[i];
+        for (int i = 0; i < N; ++i) acc[u][i] = 0.0f;
+#pragma unroll
+      for (int h = 0; h < kMaxRanks; h += 4) {
+        if (h >= p.world) break;
+        typename VT::Raw raw[U][4];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (h + q < p.world && v0 + u * stride < n) raw[u][q] = VT::load(p.peer_in[h + q], base + (v0 + u * stride) * N);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (h + q < p.world && v0 + u * stride < n) {
+              float f[N];
+              VT::unpack(raw[u][q], f);
+#pragma unroll
+              for (int i = 0; i < N; ++i) acc[u][i] += f[i];
+            }
       }
-      const auto packed = VT::pack(acc);
-      for (int q = 0; q < p.world; ++q) VT::store(p.peer_out[q], e, packed);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (v0 + u * stride >= n) continue;
+        const auto packed = VT::pack(acc[u]);
+        const long long e = base + (v0 + u * stride) * N;
+        for (int q = 0; q < p.world; ++q) VT::store(p.peer_out[q], e, packed);
+      }
     }
   }
   rank_barrier<X>(p, s, 2);
