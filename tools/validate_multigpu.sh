@@ -9,6 +9,7 @@ RUN="python -m torch.distributed.run --nnodes=1 --nproc-per-node"
 # 1. NVLS K1 parity against the oracle (single process, N devices) + the full GPU suite
 timeout 1800 python -m pytest tests -m gpu -q -x > $OUT/pytest_gpu.log 2>&1; tail -3 $OUT/pytest_gpu.log
 timeout 600 python -m pytest tests/test_k1_gpu.py -q -m gpu -k nvls_multi_gpu > $OUT/nvls_parity.log 2>&1; tail -2 $OUT/nvls_parity.log
+timeout 1800 python -m pytest tests/test_nvls_gpu.py -q -m gpu -k nvls_hw -rs > $OUT/nvls_hw.log 2>&1; tail -4 $OUT/nvls_hw.log
 # 2. bench.py at N = 2, 4, ..., N (the driver's scaling run), both arms
 for n in 2 4 8; do
   [ $n -le $N ] || continue
