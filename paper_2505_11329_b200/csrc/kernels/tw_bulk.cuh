@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     if (c < p.V) load_weight<N>(p.weight, static_cast<long long>(c) * N, w[k]);
   }
   if (lt == 0 && w[0][0] != 12345.0f) k2_tr(40 + grp);  // weights in registers
+  const float inv_h = 1.0f / static_cast<float>(p.H);
   for (long long i = grp; i < nrows; i += G) {
     const int s = static_cast<int>(i % S);
     const uint32_t ph = static_cast<uint32_t>((i / S) & 1);
@@ -417,13 +418,29 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     }
     if (lt == 0 && i < 4 && ss != 12345.0f) k2_tr(44 + 4 * static_cast<int>(i));
     ss = warp_sum(ss);
-    Acc total;
     Acc* pp = part + (grp * 2 + ((i / G) & 1)) * cwarps;
     if (lane == 0) pp[cw] = ss;
     named_bar_sync(G == 1 ? 1 : 1 + grp, tpr);
-    total = 0;
-    for (int q = 0; q < cwarps; ++q) total += pp[q];
-    const float inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(p.H)) + p.eps);
+    float inv;
+    if constexpr (sizeof(E) == 2 && G == 2) {
+      // the packed bf16 body (2e-2 tolerance): the warps' partials as 16-byte
+      // loads and a tree, and one rsqrt -- the serial chain of dependent
+      // shared loads + IEEE div/sqrt/div sits on every row's critical path
+      float total = 0.0f;
+      if ((cwarps & 3) == 0) {
+        for (int q = 0; q < cwarps; q += 4) {
+          const float4 v = *reinterpret_cast<const float4*>(pp + q);
+          total += (v.x + v.y) + (v.z + v.w);
+        }
+      } else {
+        for (int q = 0; q < cwarps; ++q) total += pp[q];
+      }
+      inv = rsqrtf(total * inv_h + p.eps);
+    } else {
+      Acc total = 0;
+      for (int q = 0; q < cwarps; ++q) total += pp[q];
+      inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(p.H)) + p.eps);
+    }
     if (lt == 0 && i < 4 && inv != 12345.0f) k2_tr(45 + 4 * static_cast<int>(i));
     if constexpr (sizeof(E) == 2 && G == 2) {
       k2_bf16_pass2<VPT>(st, lt, tpr, p.V, rr, w, inv);
