@@ -420,7 +420,14 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     ss = warp_sum(ss);
     Acc* pp = part + (grp * 2 + ((i / G) & 1)) * cwarps;
     if (lane == 0) pp[cw] = ss;
+    constexpr bool kEarlyResStore = sizeof(E) == 2 && G == 2;
+    if constexpr (kEarlyResStore) fence_proxy_async_smem();  // r' (pass 1) -> visible to the bulk engine
     named_bar_sync(G == 1 ? 1 : 1 + grp, tpr);
+    // r' is final after pass 1: its bulk store starts now and overlaps the
+    // statistic and pass 2 (committed with the output's store below)
+    if constexpr (kEarlyResStore)
+      if (storer)
+        bulk_s2g(static_cast<unsigned char*>(p.res_out) + row * p.row_bytes, st + p.row_bytes, p.row_bytes);
     float inv;
     if constexpr (sizeof(E) == 2 && G == 2) {
       // the packed bf16 body (2e-2 tolerance): the warps' partials as 16-byte
@@ -463,7 +470,8 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     if (lt == 0 && i < 4) k2_tr(47 + 4 * static_cast<int>(i));
     if (storer) {
       bulk_s2g(static_cast<unsigned char*>(p.out) + row * p.row_bytes, st, p.row_bytes);
-      bulk_s2g(static_cast<unsigned char*>(p.res_out) + row * p.row_bytes, st + p.row_bytes, p.row_bytes);
+      if constexpr (!kEarlyResStore)
+        bulk_s2g(static_cast<unsigned char*>(p.res_out) + row * p.row_bytes, st + p.row_bytes, p.row_bytes);
       bulk_commit();
       if (i < 8) k2_tr(20 + static_cast<int>(i));
       // this storer's previous row (i - G) has finished reading its stage: free
