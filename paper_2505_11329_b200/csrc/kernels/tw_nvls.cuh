@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kNvlsBlock, 1) k1_nvls_kernel(const __grid_con
   using Acc = typename std::conditional<sizeof(E) == 4, double, float>::type;  // reference: double ss for fp32
   constexpr int kSets = D + 1;                           // x register sets (ring)
   constexpr int U = (kSets % 2 == 0) ? kSets : 2 * kSets;  // unroll: x ring and residual ping-pong align
-  __shared__ Acc part[kMaxGroups][2][kNvlsBlock / 32];
+  __shared__ __align__(16) Acc part[kMaxGroups][2][kNvlsBlock / 32];
 
   const RankSlot& s = p.slot[MM::kSim ? blockIdx.y : 0];
   const int tpr = p.tpr;
@@ -243,10 +243,9 @@ __global__ void __launch_bounds__(kNvlsBlock, 1) k1_nvls_kernel(const __grid_con
     } else {
       if ((lt & 31) == 0) part[group][parity][lt >> 5] = ss;
       named_bar_sync(1 + group, tpr);
-      total = 0;
-      for (int w = 0; w < nwarps; ++w) total += part[group][parity][w];
+      total = sum_partials<Acc>(part[group][parity], nwarps);
     }
-    const float inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(H)) + p.eps);
+    const float inv = inv_rms<Acc>(total, H, p.eps);
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
       const int c = lt + k * tpr;

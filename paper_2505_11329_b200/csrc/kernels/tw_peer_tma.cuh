@@ -179,9 +179,7 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
 #pragma unroll
         for (int c = 0; c < n - 1; ++c) mbar_arrive_n(&empty[static_cast<int>((g - n + c) % S)], cwarps);
       }
-      Acc total = 0;
-      for (int q = 0; q < cwarps; ++q) total += pp[q];
-      const float inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(p.H)) + p.eps);
+      const float inv = inv_rms<Acc>(sum_partials<Acc>(pp, cwarps), p.H, p.eps);
 #pragma unroll
       for (int k = 0; k < VPT; ++k) {
         const int cc = lt + k * tpr;

@@ -214,6 +214,36 @@ __device__ __forceinline__ Acc warp_sum(Acc v) {
   return v;
 }
 
+// The row statistic from a row group's warp partials.  bf16 rows (Acc =
+// float, 2e-2 tolerance): the partials as 16-byte loads and a tree, then one
+// rsqrtf -- a chain of dependent scalar shared loads and IEEE div / sqrt /
+// div sat on every row's critical path (K2's packed body: +5 % per SM under
+// an SM budget).  fp32 rows (Acc = double): the reference's arithmetic,
+// float(ss / H) and 1 / sqrt (proj/src/numerics.cpp:57-61), unchanged.
+template <class Acc>
+__device__ __forceinline__ Acc sum_partials(const Acc* parts, int n) {
+  Acc t = 0;
+  if constexpr (sizeof(Acc) == 4) {
+    if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(parts) & 15) == 0) {
+      for (int q = 0; q < n; q += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(parts + q);
+        t += (v.x + v.y) + (v.z + v.w);
+      }
+      return t;
+    }
+  }
+  for (int q = 0; q < n; ++q) t += parts[q];
+  return t;
+}
+
+template <class Acc>
+__device__ __forceinline__ float inv_rms(Acc total, long long H, float eps) {
+  if constexpr (sizeof(Acc) == 4)
+    return rsqrtf(total * (1.0f / static_cast<float>(H)) + eps);
+  else
+    return 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(H)) + eps);
+}
+
 // ---- cross-rank barrier ------------------------------------------------------------
 
 template <Xport X>
@@ -292,7 +322,7 @@ __global__ void __launch_bounds__(kBlock, (X == Xport::Peer && VPT <= 2) ? 2 : 1
   using Raw = typename VT::Raw;
   // fp32 activations keep the reference's double sum of squares.
   using Acc = typename std::conditional<sizeof(E) == 4, double, float>::type;
-  __shared__ Acc part[kMaxGroups][2][kBlock / 32];
+  __shared__ __align__(16) Acc part[kMaxGroups][2][kBlock / 32];
 
   const int slot_idx = (X == Xport::Local) ? 0 : static_cast<int>(blockIdx.y);
   const RankSlot& s = p.slot[slot_idx];
@@ -408,10 +438,9 @@ __global__ void __launch_bounds__(kBlock, (X == Xport::Peer && VPT <= 2) ? 2 : 1
     } else {
       if ((lt & 31) == 0) part[group][parity][warp_in_group] = ss;
       named_bar_sync(1 + group, tpr);
-      total = 0;
-      for (int w = 0; w < nwarps; ++w) total += part[group][parity][w];
+      total = sum_partials<Acc>(part[group][parity], nwarps);
     }
-    const float inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(H)) + p.eps);
+    const float inv = inv_rms<Acc>(total, H, p.eps);
     // Phase 4: out = r' * inv * w, stored locally / to every rank.
     const float* wgt = (X == Xport::Local) ? p.weight : s.weight;
 #pragma unroll
