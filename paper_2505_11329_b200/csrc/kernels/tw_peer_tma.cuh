@@ -173,11 +173,21 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
       ss = warp_sum(ss);
       Acc* pp = part + (i & 1) * cwarps;
       if (lane == 0) pp[cw] = ss;
+      fence_proxy_async_smem();  // r' (written above) -> visible to the bulk engine
       named_bar_sync(1, tpr);
-      // Every consumer is past the input-only stages of this row: free them.
+      const long long grow = (p.row_offset + t) * row_bytes;
       if (storer) {
+        // Every consumer is past the input-only stages of this row: free them.
 #pragma unroll
         for (int c = 0; c < n - 1; ++c) mbar_arrive_n(&empty[static_cast<int>((g - n + c) % S)], cwarps);
+        // r' is final: its stores (the local shard, and every rank's RESIDUAL
+        // with G = 2) start now and overlap the statistic and the output pass;
+        // they are committed with the output's stores below.
+        bulk_s2g(static_cast<unsigned char*>(s.residual) + (t - row0) * row_bytes, res, row_bytes);
+        if (p.flags & kGatherResidual) {
+#pragma unroll
+          for (int q = 0; q < W; ++q) bulk_s2g(static_cast<unsigned char*>(p.peer_res[q]) + grow, res, row_bytes);
+        }
       }
       const float inv = inv_rms<Acc>(sum_partials<Acc>(pp, cwarps), p.H, p.eps);
 #pragma unroll
@@ -194,13 +204,8 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
       fence_proxy_async_smem();
       named_bar_sync(1, tpr);
       if (storer) {
-        const long long grow = (p.row_offset + t) * row_bytes;
-        bulk_s2g(static_cast<unsigned char*>(s.residual) + (t - row0) * row_bytes, res, row_bytes);
 #pragma unroll
-        for (int q = 0; q < W; ++q) {
-          bulk_s2g(static_cast<unsigned char*>(p.peer_out[q]) + grow, stg, row_bytes);
-          if (p.flags & kGatherResidual) bulk_s2g(static_cast<unsigned char*>(p.peer_res[q]) + grow, res, row_bytes);
-        }
+        for (int q = 0; q < W; ++q) bulk_s2g(static_cast<unsigned char*>(p.peer_out[q]) + grow, stg, row_bytes);
         bulk_commit();
         if (lazy) {
           if (prev_last >= 0) {
