@@ -250,9 +250,13 @@ def test_weave_outputs_equal_sequential(cuda, T, split, graph):
         states[mode] = _read_state(r, T)
     want_R, want_X = _layer_model(R0, w, I, executed)
     for mode, (R, X) in states.items():
-        # the unfused baseline's RMSNorm kernel (fp32 sum of squares, rsqrtf)
-        # drifts by up to ~1.1x the 2e-2 bar over five chained layers
-        rel = 3e-2 if mode == "unfused" else 2e-2
+        # Five chained bf16 layers against an fp32 model: one op stays within
+        # north_star's 2e-2 (tests/test_k2_gpu.py), but bf16 roundings of R
+        # and X compound from layer to layer, and a row statistic taken with
+        # rsqrtf (the unfused baseline's RMSNorm, K2's packed two-group body)
+        # moved the worst element to ~1.1x that bar.  A schedule error -- an op
+        # on the wrong rows or before its producer -- is an O(1) error.
+        rel = 3e-2
         assert_bf16_close(R, want_R, rel=rel, what=f"{mode} residual vs model")
         assert_bf16_close(X, want_X, rel=rel, what=f"{mode} hidden vs model")
     # the weave against the sequential fused schedule it reorders
