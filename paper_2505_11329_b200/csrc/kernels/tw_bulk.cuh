@@ -28,8 +28,14 @@ __device__ __forceinline__ void k2_tr(int slot) {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   if (slot < 64) k2_trace[blockIdx.x * 64 + slot] = t;
 }
+// k2_tr after `dep` has been computed (the empty asm consumes it first).
+__device__ __forceinline__ void k2_tr_after(int slot, float dep) {
+  asm volatile("" ::"f"(dep));
+  k2_tr(slot);
+}
 #else
 __device__ __forceinline__ void k2_tr(int) {}
+__device__ __forceinline__ void k2_tr_after(int, float) {}
 #endif
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -385,7 +391,7 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
     const int c = lt + k * tpr;
     if (c < p.V) load_weight<N>(p.weight, static_cast<long long>(c) * N, w[k]);
   }
-  if (lt == 0 && w[0][0] != 12345.0f) k2_tr(40 + grp);  // weights in registers
+  if (lt == 0) k2_tr_after(40 + grp, w[0][0]);  // weights in registers
   const float inv_h = 1.0f / static_cast<float>(p.H);
   for (long long i = grp; i < nrows; i += G) {
     const int s = static_cast<int>(i % S);
@@ -416,7 +422,7 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
         }
       }
     }
-    if (lt == 0 && i < 4 && ss != 12345.0f) k2_tr(44 + 4 * static_cast<int>(i));
+    if (lt == 0 && i < 4) k2_tr_after(44 + 4 * static_cast<int>(i), static_cast<float>(ss));
     ss = warp_sum(ss);
     Acc* pp = part + (grp * 2 + ((i / G) & 1)) * cwarps;
     if (lane == 0) pp[cw] = ss;
@@ -448,7 +454,7 @@ __global__ void __launch_bounds__(kBulkMaxConsumers + 32, 1) k2_tma_kernel(const
       for (int q = 0; q < cwarps; ++q) total += pp[q];
       inv = 1.0f / sqrtf(static_cast<float>(total / static_cast<Acc>(p.H)) + p.eps);
     }
-    if (lt == 0 && i < 4 && inv != 12345.0f) k2_tr(45 + 4 * static_cast<int>(i));
+    if (lt == 0 && i < 4) k2_tr_after(45 + 4 * static_cast<int>(i), inv);
     if constexpr (sizeof(E) == 2 && G == 2) {
       k2_bf16_pass2<VPT>(st, lt, tpr, p.V, rr, w, inv);
     } else {
