@@ -106,3 +106,25 @@ def test_comm_requires_a_device_here():
         pytest.skip("GPU visible")
     with pytest.raises(tw.CudaError):
         tw.Communicator(2, [0, 0], 1 << 20)
+
+
+def test_staged_copies_validate_on_the_host():
+    """tw_memcpy_h2d_staged / tw_memcpy_d2h_staged reject bad arguments before
+    any device work: null buffers and partial elements (DIMENSION), unknown
+    dtypes and a destination / source that is not device memory (CONFIG; on
+    a GPU-less host every pointer is host memory); zero bytes is a no-op."""
+    import ctypes
+    from paper_2505_11329_b200 import _lib
+    L = _lib.lib
+    buf = (ctypes.c_float * 16)()
+    p = ctypes.cast(buf, ctypes.c_void_p)
+    nf = ctypes.c_int(7)
+    assert L.tw_memcpy_h2d_staged(p, p, 0, _lib.TW_F32, 0, ctypes.byref(nf)) == _lib.TW_OK and nf.value == 0
+    assert L.tw_memcpy_h2d_staged(None, p, 16, _lib.TW_F32, 0, None) == _lib.TW_ERR_DIMENSION
+    assert L.tw_memcpy_h2d_staged(p, p, 6, _lib.TW_F32, 0, None) == _lib.TW_ERR_DIMENSION
+    assert L.tw_memcpy_h2d_staged(p, p, 16, 7, 0, None) == _lib.TW_ERR_CONFIG
+    assert L.tw_memcpy_h2d_staged(p, p, 16, _lib.TW_F32, 0, None) == _lib.TW_ERR_CONFIG
+    assert b"not device memory" in L.tw_last_error()
+    assert L.tw_memcpy_d2h_staged(p, None, 16) == _lib.TW_ERR_DIMENSION
+    assert L.tw_memcpy_d2h_staged(p, p, 16) == _lib.TW_ERR_CONFIG
+    assert L.tw_memcpy_d2h_staged(p, p, 0) == _lib.TW_OK
