@@ -313,23 +313,36 @@ cudaError_t launch_count_nonfinite(const void* x, long long n, bool bf16, int* c
 namespace {
 using PeerTmaFn = void (*)(RowParams);
 
-template <class E, int W>
+template <class E, int W, int G = 1>
 PeerTmaFn pick_peer_tma_w(int vpt) {
   vpt = vpt <= 1 ? 1 : vpt <= 2 ? 2 : vpt <= 4 ? 4 : 0;  // c < V guards the rest
   switch (vpt) {
-    case 1: return k1_peer_tma_kernel<E, 1, W>;
-    case 2: return k1_peer_tma_kernel<E, 2, W>;
-    case 4: return k1_peer_tma_kernel<E, 4, W>;
+    case 1: return k1_peer_tma_kernel<E, 1, W, G>;
+    case 2: return k1_peer_tma_kernel<E, 2, W, G>;
+    case 4: return k1_peer_tma_kernel<E, 4, W, G>;
     default: return nullptr;
   }
 }
 
+// Consumer row groups of the PEER engine.  Two groups (two rows in flight
+// per CTA) pay at world 2 -- co-located TP=2, bf16, T=8192, 8 SMs: H=8192
+// 635 -> 553 us, H=4096 473 -> 344 us; never slower beyond noise at larger
+// budgets -- while world 3 loses its third stage to the even-ring rule
+// (S=2) and is slower (profiles/k2_packed_ab_r02.txt section 16).
+// TW_K1_PEER_GROUPS=1|2 forces the choice (world <= 3).
+int peer_tma_groups(int world, int /*blocks*/) {
+  static const char* env = std::getenv("TW_K1_PEER_GROUPS");
+  if (world > 3) return 1;
+  if (env && (env[0] == '1' || env[0] == '2')) return env[0] - '0';
+  return world == 2 ? 2 : 1;
+}
+
 // Worlds 2, 3, 4 (one stage per row) and 8 (two); others use the row engine.
 template <class E>
-PeerTmaFn pick_peer_tma(int world, int vpt) {
+PeerTmaFn pick_peer_tma(int world, int vpt, int G) {
   switch (world) {
-    case 2: return pick_peer_tma_w<E, 2>(vpt);
-    case 3: return pick_peer_tma_w<E, 3>(vpt);
+    case 2: return G == 2 ? pick_peer_tma_w<E, 2, 2>(vpt) : pick_peer_tma_w<E, 2>(vpt);
+    case 3: return G == 2 ? pick_peer_tma_w<E, 3, 2>(vpt) : pick_peer_tma_w<E, 3>(vpt);
     case 4: return pick_peer_tma_w<E, 4>(vpt);
     case 8: return pick_peer_tma_w<E, 8>(vpt);
     default: return nullptr;
@@ -337,43 +350,58 @@ PeerTmaFn pick_peer_tma(int world, int vpt) {
 }
 
 // Ring depth under a 200 KB shared-memory budget: peer_tma_stage_rows(W)
-// rows per stage, 2..4 stages (0 = the shape does not fit).
-bool peer_tma_geometry(int world, long long H, bool bf16, int* stages, size_t* smem) {
+// rows per stage, 2..4 stages, a multiple of the row groups (0 = the shape
+// does not fit).
+bool peer_tma_geometry(int world, int G, long long H, bool bf16, int* stages, size_t* smem) {
   const size_t row = static_cast<size_t>(H) * (bf16 ? 2 : 4);
   const size_t stage = peer_tma_stage_rows(world) * row;
   static const char* env = std::getenv("TW_K1_PEER_STAGES");  // A/B: ring depth cap
   const int cap = env ? std::max(2, std::atoi(env)) : 4;
-  const int S = static_cast<int>(std::min<size_t>(cap, (200 * 1024) / stage));
+  int S = static_cast<int>(std::min<size_t>(cap, (200 * 1024) / stage));
+  S -= S % G;  // each row group's stages are its own (k1_peer_tma_kernel)
   if (S < 2) return false;
   *stages = S;
-  *smem = S * stage + 2 * S * sizeof(uint64_t) + 2 * 8 * sizeof(double);
+  *smem = S * stage + 2 * S * sizeof(uint64_t) + G * 2 * 8 * sizeof(double);
   return true;
 }
 }  // namespace
 
+// Resident CTAs per SM of the engine a launch may pick: the minimum over the
+// one- and two-group kernels (the grid is sized before the group count is
+// chosen, and co-located ranks need every CTA resident for the rank barrier).
 int k1_peer_tma_blocks_per_sm(int world, int V, long long H, bool bf16) {
   const int vpt = (V + 255) / 256;
-  PeerTmaFn fn = bf16 ? pick_peer_tma<uint16_t>(world, vpt) : pick_peer_tma<float>(world, vpt);
-  int S = 0;
-  size_t smem = 0;
-  if (!fn || !peer_tma_geometry(world, H, bf16, &S, &smem)) return 0;
-  if (ensure_dynamic_smem(reinterpret_cast<const void*>(fn), smem) != cudaSuccess) return 0;
-  return cached_occupancy(reinterpret_cast<const void*>(fn), 288, smem);
+  int occ = 0;
+  for (int G = 1; G <= (world <= 3 ? 2 : 1); ++G) {
+    PeerTmaFn fn = bf16 ? pick_peer_tma<uint16_t>(world, vpt, G) : pick_peer_tma<float>(world, vpt, G);
+    int S = 0;
+    size_t smem = 0;
+    if (!fn || !peer_tma_geometry(world, G, H, bf16, &S, &smem)) {
+      if (G == 1) return 0;
+      continue;  // the launcher falls back to one group
+    }
+    if (ensure_dynamic_smem(reinterpret_cast<const void*>(fn), smem) != cudaSuccess) return 0;
+    const int o = cached_occupancy(reinterpret_cast<const void*>(fn), G * 256 + 32, smem);
+    occ = G == 1 ? o : std::min(occ, o);
+  }
+  return occ;
 }
 
 cudaError_t launch_k1_peer_tma(RowParams params, int world, int V, bool bf16, dim3 grid, cudaStream_t stream) {
   const int vpt = (V + 255) / 256;
-  PeerTmaFn fn = bf16 ? pick_peer_tma<uint16_t>(world, vpt) : pick_peer_tma<float>(world, vpt);
+  int G = peer_tma_groups(world, static_cast<int>(grid.x));
   int S = 0;
   size_t smem = 0;
-  if (!fn || !peer_tma_geometry(world, params.H, bf16, &S, &smem)) return cudaErrorNotSupported;
+  if (G > 1 && !peer_tma_geometry(world, G, params.H, bf16, &S, &smem)) G = 1;
+  PeerTmaFn fn = bf16 ? pick_peer_tma<uint16_t>(world, vpt, G) : pick_peer_tma<float>(world, vpt, G);
+  if (!fn || !peer_tma_geometry(world, G, params.H, bf16, &S, &smem)) return cudaErrorNotSupported;
   cudaError_t e = ensure_dynamic_smem(reinterpret_cast<const void*>(fn), smem);
   if (e != cudaSuccess) return e;
   params.V = V;
   params.nslots_stages = S;
   params.world = world;
   void* args[] = {&params};
-  return cudaLaunchKernel(reinterpret_cast<const void*>(fn), grid, dim3(288), args, smem, stream);
+  return cudaLaunchKernel(reinterpret_cast<const void*>(fn), grid, dim3(G * 256 + 32), args, smem, stream);
 }
 
 }  // namespace tw

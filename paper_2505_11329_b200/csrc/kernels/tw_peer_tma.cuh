@@ -33,8 +33,12 @@ __host__ __device__ constexpr int peer_tma_stage_rows(int W) {
   return (W + 1 + peer_tma_chunks(W) - 1) / peer_tma_chunks(W);
 }
 
-template <class E, int VPT, int W>
-__global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_constant__ RowParams p) {
+// G consumer row groups (G = 2 only with one stage per token row, W <= 3):
+// group g takes the CTA's rows i = g, g + G, ...; a group frees its stage as
+// soon as its stores have read it when the ring has no spare stages for a
+// one-row lag.
+template <class E, int VPT, int W, int G = 1>
+__global__ void __launch_bounds__(G * 256 + 32, 1) k1_peer_tma_kernel(const __grid_constant__ RowParams p) {
   constexpr int N = 16 / sizeof(E);
   using VT = Vec<E, N>;
   using Acc = typename std::conditional<sizeof(E) == 4, double, float>::type;
@@ -52,11 +56,15 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
   // With more stages than chunks the final stage of a row is released one row
   // late (after the next row's stores are issued); otherwise that would block
   // the producer's next row, so the storer waits for its own reads instead.
-  const bool lazy = S > n;
+  // A parity wait names a phase only if the waiter consumed the stage's
+  // previous phase: row i - S must be the group's own row, so S % G == 0
+  // (the launcher rounds S down).
+  static_assert(G == 1 || peer_tma_chunks(W) == 1, "two row groups need one stage per token row");
+  const bool lazy = G == 1 ? S > n : S >= 2 * G + 1;
   unsigned char* ring = smem;  // [S][R rows]
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(S) * stage_bytes);
   uint64_t* empty = full + S;
-  Acc* part = reinterpret_cast<Acc*>(empty + S);  // [2][8 consumer warps]
+  Acc* part = reinterpret_cast<Acc*>(empty + S);  // [G][2][8 consumer warps]
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
@@ -100,18 +108,20 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
       }
     }
   } else {
-    const int lt = threadIdx.x - 32;
+    const int grp = G == 1 ? 0 : (threadIdx.x - 32) / tpr;
+    const int lt = threadIdx.x - 32 - grp * tpr;
     const int cw = lt >> 5;
     const bool storer = lt == 0;
+    part += grp * 2 * cwarps;
     float w[VPT][N];
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
       const int c = lt + k * tpr;
       if (c < p.V) load_weight<N>(s.weight, static_cast<long long>(c) * N, w[k]);
     }
-    long long g = 0;
-    int prev_last = -1;  // final stage of the previous row (lazy release)
-    for (long long i = 0; i < nrows; ++i) {
+    int prev_last = -1;  // final stage of this group's previous row (lazy release)
+    for (long long i = grp; i < nrows; i += G) {
+      long long g = i * n;  // stage sequence number of the row's first chunk
       const long long t = row0 + blockIdx.x + i * stride;
       float x[VPT][N];
 #pragma unroll
@@ -174,7 +184,7 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
       Acc* pp = part + (i & 1) * cwarps;
       if (lane == 0) pp[cw] = ss;
       fence_proxy_async_smem();  // r' (written above) -> visible to the bulk engine
-      named_bar_sync(1, tpr);
+      named_bar_sync(1 + grp, tpr);
       const long long grow = (p.row_offset + t) * row_bytes;
       if (storer) {
         // Every consumer is past the input-only stages of this row: free them.
@@ -202,7 +212,7 @@ __global__ void __launch_bounds__(256 + 32, 1) k1_peer_tma_kernel(const __grid_c
         }
       }
       fence_proxy_async_smem();
-      named_bar_sync(1, tpr);
+      named_bar_sync(1 + grp, tpr);
       if (storer) {
 #pragma unroll
         for (int q = 0; q < W; ++q) bulk_s2g(static_cast<unsigned char*>(p.peer_out[q]) + grow, stg, row_bytes);

@@ -218,6 +218,71 @@ def test_k1_repeated_launches_and_budgets(cuda, orc):
 
 
 @pytest.mark.parametrize("dtype_name", ["float32", "bfloat16"])
+@pytest.mark.parametrize("H", [1024, 4096, 8192])
+def test_k1_world2_row_groups_across_budgets(cuda, orc, dtype_name, H):
+    """World 2 runs the PEER engine with two consumer row groups
+    (tw_launch.cu peer_tma_groups): parity at budgets from one CTA (every
+    row of a rank in one CTA, odd and even counts) to the full grid, one
+    communicator across launches."""
+    import torch
+    import paper_2505_11329_b200 as tw
+    W = 2
+    dtype = getattr(torch, dtype_name)
+    bf16 = dtype == torch.bfloat16
+    comm = tw.Communicator(W, [0] * W, 301 * H * 4, tw.TW_TRANSPORT_PEER)
+    for it, (T, budget) in enumerate([(301, 1), (300, 2), (77, 8), (64, 74), (150, 75), (301, 148), (5, 16)]):
+        inputs, residual, weight = group_inputs(31 * it + H, W, T, H)
+        ranges = tw.token_shard_map(T, W)
+        inputs, residual, want_out, want_res = oracle_case(orc, inputs, residual, weight, ranges, bf16)
+        outs, res, gathered = run_k1(inputs, residual, weight, dtype, gather=True, sm_budget=budget, comm=comm)
+        full_res = np.concatenate([bf16_round(x) if bf16 else x for x in want_res])
+        for r in range(W):
+            if bf16:
+                assert_bf16_close(outs[r], want_out, what=f"budget {budget} rank {r} output")
+                assert np.array_equal(res[r], bf16_round(want_res[r])), f"budget {budget} rank {r} residual"
+            else:
+                assert_abs_close(outs[r], want_out, 1e-5, f"budget {budget} rank {r} output")
+                assert np.array_equal(res[r], want_res[r]), f"budget {budget} rank {r} residual"
+            assert np.array_equal(gathered[r], full_res), f"budget {budget} rank {r} gathered residual"
+    comm.check()
+    comm.close()
+
+
+_FORCED_GROUPS = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+import paper_2505_11329_b200 as tw
+from tests.helpers import group_inputs, bf16_round
+from tests.test_k1_gpu import run_k1, oracle_case
+import oracle
+orc = oracle.Oracle()
+for W, H, T, budget in [(2, 8192, 97, 4), (2, 1024, 200, 148), (3, 8192, 97, 4), (3, 2048, 64, 3), (3, 512, 33, 98)]:
+    inputs, residual, weight = group_inputs(W * 7 + H + T, W, T, H)
+    ranges = tw.token_shard_map(T, W)
+    inputs, residual, want_out, want_res = oracle_case(orc, inputs, residual, weight, ranges, False)
+    outs, res, _ = run_k1(inputs, residual, weight, torch.float32, sm_budget=budget)
+    for r in range(W):
+        assert np.abs(outs[r] - want_out).max() <= 1e-5, (W, H, T, r)
+        assert np.array_equal(res[r], want_res[r]), (W, H, T, r)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("groups", ["1", "2"])
+def test_k1_peer_forced_row_groups(cuda, groups):
+    """TW_K1_PEER_GROUPS forces one or two row groups for worlds 2 and 3 (the
+    env is read once per process, so each setting runs in its own)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TW_K1_PEER_GROUPS=groups)
+    out = subprocess.run([sys.executable, "-c", _FORCED_GROUPS], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("dtype_name", ["float32", "bfloat16"])
 def test_k1_baseline_config0(cuda, orc, dtype_name):
     """BASELINE.json configs[0]: 2 ranks, 1024 tokens x 4096 hidden, vs the
     oracle on the same inputs (the reference's CPU-runnable case)."""
