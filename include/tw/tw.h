@@ -127,6 +127,17 @@ TW_API tw_status tw_rmsnorm_residual_host_sync(const void* h_input, const void* 
                                                void* h_output, const float* h_weight, int64_t T, int64_t H,
                                                float eps, tw_dtype dtype, unsigned flags);
 
+/* tw_rmsnorm_residual_host_sync whose destination rows may still be in
+ * preparation: rows_ready[0..n_ready-1] are row counters the caller advances
+ * (release stores / __atomic_store_n) from other threads; chunk k's results
+ * are copied into h_output / h_residual_out only once every counter has
+ * reached the chunk's last row, so the caller's value-initialisation of the
+ * destination overlaps the transfers.  Counters must reach T. */
+TW_API tw_status tw_rmsnorm_residual_host_sync_gated(const void* h_input, const void* h_residual,
+                                                     void* h_residual_out, void* h_output, const float* h_weight,
+                                                     int64_t T, int64_t H, float eps, tw_dtype dtype,
+                                                     unsigned flags, const int64_t* rows_ready, int n_ready);
+
 /* Device-side finite scan: *nonfinite_count (device int32) += #NaN/Inf in x.
  * Replaces TokenMatrix::validate's isfinite loop (numerics.cpp:25-27). */
 TW_API tw_status tw_count_nonfinite(const void* x, int64_t n, tw_dtype dtype, int* nonfinite_count_dev, void* stream);

@@ -320,7 +320,17 @@ extern "C" {
 tw_status tw_rmsnorm_residual_host_sync(const void* h_input, const void* h_residual, void* h_residual_out,
                                         void* h_output, const float* h_weight, int64_t T, int64_t H, float eps,
                                         tw_dtype dtype, unsigned flags) {
+  return tw_rmsnorm_residual_host_sync_gated(h_input, h_residual, h_residual_out, h_output, h_weight, T, H, eps,
+                                             dtype, flags, nullptr, 0);
+}
+
+tw_status tw_rmsnorm_residual_host_sync_gated(const void* h_input, const void* h_residual, void* h_residual_out,
+                                              void* h_output, const float* h_weight, int64_t T, int64_t H,
+                                              float eps, tw_dtype dtype, unsigned flags, const int64_t* rows_ready,
+                                              int n_ready) {
   clear_error();
+  if (n_ready < 0 || (n_ready > 0 && !rows_ready))
+    return fail(TW_ERR_DIMENSION, "rmsnorm_residual_host_sync: bad rows_ready gate");
   if (T < 0 || H < 1) return fail(TW_ERR_DIMENSION, "rmsnorm_residual_host_sync: requires T >= 0 and H >= 1");
   if (!(eps > 0.0f) && eps != 0.0f)
     return fail(TW_ERR_NUMERIC, "rmsnorm_residual_host_sync: epsilon must be nonnegative");
@@ -386,6 +396,13 @@ tw_status tw_rmsnorm_residual_host_sync(const void* h_input, const void* h_resid
     if (ee != cudaSuccess) return drain(cuda_fail(ee, "host_sync: D2H"));
     size_t off, nb;
     span(k, &off, &nb);
+    // the caller may still be preparing the destination rows (the drop-in
+    // value-initialises its result vectors on helper threads): wait until
+    // every gate covers this chunk
+    const int64_t need = std::min(T, (k + 1) * chunk_rows);
+    for (int i = 0; i < n_ready; ++i)
+      for (int spins = 0; __atomic_load_n(rows_ready + i, __ATOMIC_ACQUIRE) < need; ++spins)
+        if (spins < 4096) cpu_relax(); else std::this_thread::yield();
     pcopy(hout + off, static_cast<const char*>(g.h[s][2]), hro + off, static_cast<const char*>(g.h[s][3]), nb,
           false);
     return TW_OK;

@@ -7,12 +7,14 @@
 //   all_reduce/reduce_scatter-> tw_allreduce_group (K3)
 // There is no CPU compute fallback: without a GPU these throw DeviceError.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 
 #include "tw/tw.h"
 #include "weavesim/collectives.hpp"
@@ -22,6 +24,10 @@
 namespace weavesim {
 
 namespace {
+
+// result matrices at least this large are value-initialised on helper threads
+// overlapped with the transfers (rmsnorm_residual below)
+constexpr size_t kOverlapFillBytes = 16u << 20;
 
 [[noreturn]] void throw_status(tw_status st, const std::string& where) {
   const std::string msg = where + ": " + tw_last_error();
@@ -176,20 +182,62 @@ NormResult rmsnorm_residual(const TokenMatrix& input, const TokenMatrix& residua
   }
   const std::int64_t T = input.num_tokens, H = input.hidden;
   NormResult result;
-  // The two fresh result matrices are value-initialised here, on the calling
-  // thread: a second thread would allocate from its own glibc arena, which
-  // measured 5x slower for 256 MiB blocks than the main heap.
-  result.output = TokenMatrix::zeros(T, H);
-  result.residual_out = TokenMatrix::zeros(T, H);
-  if (T == 0) return result;
+  const size_t n = static_cast<size_t>(T * H);
+  if (n * sizeof(float) < kOverlapFillBytes) {
+    result.output = TokenMatrix::zeros(T, H);
+    result.residual_out = TokenMatrix::zeros(T, H);
+    if (T == 0) return result;
+    device_count_or_throw();
+    std::lock_guard<std::mutex> lock(g_mu);
+    // Host matrices in, host matrices out: pinned-ring staging by host threads
+    // around the chunked H2D | K2 | D2H pipeline.
+    const tw_status st = tw_rmsnorm_residual_host_sync(input.values.data(), residual.values.data(),
+                                                       result.residual_out.values.data(), result.output.values.data(),
+                                                       params.weight.data(), T, H, params.epsilon, TW_F32,
+                                                       TW_HOST_CHECK_FINITE);
+    if (st == TW_ERR_NUMERIC) throw NumericError("TokenMatrix contains NaN/Inf");
+    check(st, "rmsnorm_residual");
+    return result;
+  }
   device_count_or_throw();
-  std::lock_guard<std::mutex> lock(g_mu);
-  // Host matrices in, host matrices out: pinned-ring staging by host threads
-  // around the chunked H2D | K2 | D2H pipeline.
-  const tw_status st = tw_rmsnorm_residual_host_sync(input.values.data(), residual.values.data(),
-                                                     result.residual_out.values.data(), result.output.values.data(),
-                                                     params.weight.data(), T, H, params.epsilon, TW_F32,
-                                                     TW_HOST_CHECK_FINITE);
+  // The two fresh result matrices (TokenMatrix::zeros in the reference) are
+  // allocated here, on the calling thread -- a second thread would allocate
+  // from its own glibc arena, measured 5x slower for 256 MiB blocks -- and
+  // value-initialised by two helper threads in ~4 MiB steps while the
+  // pipeline stages, transfers and computes (2 x ~18 ms of single-thread
+  // zero-fill at 8192 x 8192 that used to precede it).  resize() within the
+  // reserved capacity never reallocates, so the row pointers taken below
+  // stay valid; the pipeline copies chunk k's results in only once both
+  // fills have published rows past it (tw_rmsnorm_residual_host_sync_gated).
+  for (TokenMatrix* m : {&result.output, &result.residual_out}) {
+    m->num_tokens = T;
+    m->hidden = H;
+    m->values.reserve(n);
+  }
+  float* out = result.output.values.data();
+  float* res_out = result.residual_out.values.data();
+  alignas(64) std::int64_t ready[2] = {0, 0};
+  std::atomic<bool> stop{false};
+  const std::int64_t step = std::max<std::int64_t>(1, static_cast<std::int64_t>((4u << 20) / (H * sizeof(float))));
+  auto fill = [&](std::vector<float>* v, std::int64_t* rows) {
+    for (std::int64_t t = 0; t < T && !stop.load(std::memory_order_relaxed);) {
+      t = std::min(T, t + step);
+      v->resize(static_cast<size_t>(t * H));
+      __atomic_store_n(rows, t, __ATOMIC_RELEASE);
+    }
+  };
+  std::thread f0(fill, &result.output.values, &ready[0]);
+  std::thread f1(fill, &result.residual_out.values, &ready[1]);
+  tw_status st;
+  {
+    std::lock_guard<std::mutex> lock(g_mu);
+    st = tw_rmsnorm_residual_host_sync_gated(input.values.data(), residual.values.data(), res_out, out,
+                                             params.weight.data(), T, H, params.epsilon, TW_F32,
+                                             TW_HOST_CHECK_FINITE, ready, 2);
+  }
+  if (st != TW_OK) stop.store(true, std::memory_order_relaxed);
+  f0.join();
+  f1.join();
   if (st == TW_ERR_NUMERIC) throw NumericError("TokenMatrix contains NaN/Inf");
   check(st, "rmsnorm_residual");
   return result;

@@ -154,7 +154,10 @@ void host_cases() {
 void gpu_cases() {
   // test_numerics.cpp:62-89 -- vs an independent double-precision restatement
   std::mt19937_64 rng(7);
-  for (auto [T, H] : {std::pair<std::int64_t, std::int64_t>{1, 8}, {5, 16}, {17, 33}, {64, 128}}) {
+  // 2049 x 4096 fp32 (32 MiB per matrix): the result vectors are
+  // value-initialised on helper threads overlapped with the pipeline (ragged
+  // against both the 512-row pipeline chunk and the 256-row fill step)
+  for (auto [T, H] : {std::pair<std::int64_t, std::int64_t>{1, 8}, {5, 16}, {17, 33}, {64, 128}, {2049, 4096}}) {
     const TokenMatrix in = random_matrix(T, H, rng, -2.f, 2.f);
     const TokenMatrix res = random_matrix(T, H, rng, -2.f, 2.f);
     NormParams params;
@@ -177,6 +180,20 @@ void gpu_cases() {
       }
     }
     CHECK(ok);
+  }
+  {
+    // a NaN on the overlapped-fill path: NumericError, helper threads joined,
+    // and the next call on the same path is correct
+    TokenMatrix in = random_matrix(1500, 4096, rng, -1.f, 1.f);
+    const TokenMatrix res = random_matrix(1500, 4096, rng, -1.f, 1.f);
+    NormParams p = unit_norm(4096);
+    in.at(1400, 7) = std::nanf("");
+    CHECK_THROWS_AS(rmsnorm_residual(in, res, p), NumericError);
+    in.at(1400, 7) = 0.5f;
+    const NormResult r = rmsnorm_residual(in, res, p);
+    bool same = r.output.values.size() == in.values.size() && r.residual_out.values.size() == in.values.size();
+    for (size_t i = 0; same && i < in.values.size(); ++i) same = r.residual_out.values[i] == in.values[i] + res.values[i];
+    CHECK(same);
   }
   // test_numerics.cpp:91-98
   NormParams p8 = unit_norm(8);
