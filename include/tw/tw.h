@@ -127,24 +127,16 @@ TW_API tw_status tw_rmsnorm_residual_host_sync(const void* h_input, const void* 
                                                void* h_output, const float* h_weight, int64_t T, int64_t H,
                                                float eps, tw_dtype dtype, unsigned flags);
 
-/* tw_rmsnorm_residual_host_sync that hands the results to the caller instead
- * of copying them into h_output / h_residual_out (both may be NULL): once
- * chunk k's output and residual_out rows are in pinned host memory, `sink`
- * is called on the calling thread with (ctx, row0, rows, output, residual_out),
- * in row order, and must return without blocking.  The two windows stay
- * valid until every rows_consumed[0..n_consumed-1] counter (advanced by the
- * caller's consumers with release stores / __atomic_store_n) has reached
- * row0 + rows; the call returns once every counter has reached T.  This lets
- * a caller construct its destination from the results directly (the
- * drop-in appends them to fresh std::vectors instead of zero-filling those
- * first).  Errors as tw_rmsnorm_residual_host_sync; after an error the
- * caller must stop waiting for further chunks. */
-typedef void (*tw_rows_sink)(void* ctx, int64_t row0, int64_t rows, const void* output, const void* residual_out);
-TW_API tw_status tw_rmsnorm_residual_host_sync_sink(const void* h_input, const void* h_residual,
-                                                    void* h_residual_out, void* h_output, const float* h_weight,
-                                                    int64_t T, int64_t H, float eps, tw_dtype dtype, unsigned flags,
-                                                    tw_rows_sink sink, void* sink_ctx, const int64_t* rows_consumed,
-                                                    int n_consumed);
+/* tw_rmsnorm_residual_host_sync whose destination rows may still be in
+ * preparation: rows_ready[0..n_ready-1] are row counters the caller advances
+ * (release stores / __atomic_store_n) from other threads; chunk k's results
+ * are copied into h_output / h_residual_out only once every counter has
+ * reached the chunk's last row, so the caller's value-initialisation of the
+ * destination overlaps the transfers.  Counters must reach T. */
+TW_API tw_status tw_rmsnorm_residual_host_sync_gated(const void* h_input, const void* h_residual,
+                                                     void* h_residual_out, void* h_output, const float* h_weight,
+                                                     int64_t T, int64_t H, float eps, tw_dtype dtype,
+                                                     unsigned flags, const int64_t* rows_ready, int n_ready);
 
 /* Device-side finite scan: *nonfinite_count (device int32) += #NaN/Inf in x.
  * Replaces TokenMatrix::validate's isfinite loop (numerics.cpp:25-27). */

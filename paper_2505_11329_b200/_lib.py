@@ -88,9 +88,9 @@ _SIGNATURES = [
      [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_int, c_int64, c_void_p]),
     ("tw_rmsnorm_residual_host_sync", c_int,
      [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_int, c_uint]),
-    ("tw_rmsnorm_residual_host_sync_sink", c_int,
+    ("tw_rmsnorm_residual_host_sync_gated", c_int,
      [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_float, c_int, c_uint,
-      c_void_p, c_void_p, POINTER(c_int64), c_int]),
+      POINTER(c_int64), c_int]),
     ("tw_count_nonfinite", c_int, [c_void_p, c_int64, c_int, c_void_p, c_void_p]),
     ("tw_token_shard_map", c_int, [c_int64, c_int, POINTER(c_int64)]),
     ("tw_shard_map_validate", c_int, [POINTER(c_int64), c_int, c_int64]),

@@ -280,35 +280,12 @@ bool copy_check(void* dst, const void* src, size_t bytes, bool bf16, bool check)
   return bad != 0;
 }
 
-// Sink mode hands each chunk's results to the caller in a pinned window and
-// reuses the window only once the caller has consumed it: twice the in-ring's
-// depth, so a consumer one chunk behind does not stall the transfers.
-constexpr int kOutSlots = 2 * kSlots;
-
 struct PinnedRing {
   int device = -1;
   size_t chunk = 0;
   void* h[kSlots][4] = {};  // pinned in, res, out, res_out
   cudaEvent_t drained[kSlots] = {};
-  size_t ochunk = 0;
-  void* ho[kOutSlots][2] = {};  // sink mode: pinned out, res_out windows
 };
-
-tw_status ensure_out_windows(PinnedRing& g, size_t chunk) {
-  if (g.ochunk >= chunk) return TW_OK;
-  for (int i = 0; i < kOutSlots; ++i)
-    for (int j = 0; j < 2; ++j) {
-      if (g.ho[i][j]) cudaFreeHost(g.ho[i][j]);
-      g.ho[i][j] = nullptr;
-      cudaError_t e = cudaHostAlloc(&g.ho[i][j], chunk, cudaHostAllocDefault);
-      if (e != cudaSuccess) {
-        g.ochunk = 0;
-        return cuda_fail(e, "host_sync: cudaHostAlloc(out windows)");
-      }
-    }
-  g.ochunk = chunk;
-  return TW_OK;
-}
 PinnedRing g_ring[64];
 
 tw_status ensure_ring(PinnedRing& g, int dev, size_t chunk) {
@@ -343,23 +320,23 @@ extern "C" {
 tw_status tw_rmsnorm_residual_host_sync(const void* h_input, const void* h_residual, void* h_residual_out,
                                         void* h_output, const float* h_weight, int64_t T, int64_t H, float eps,
                                         tw_dtype dtype, unsigned flags) {
-  return tw_rmsnorm_residual_host_sync_sink(h_input, h_residual, h_residual_out, h_output, h_weight, T, H, eps,
-                                            dtype, flags, nullptr, nullptr, nullptr, 0);
+  return tw_rmsnorm_residual_host_sync_gated(h_input, h_residual, h_residual_out, h_output, h_weight, T, H, eps,
+                                             dtype, flags, nullptr, 0);
 }
 
-tw_status tw_rmsnorm_residual_host_sync_sink(const void* h_input, const void* h_residual, void* h_residual_out,
-                                             void* h_output, const float* h_weight, int64_t T, int64_t H, float eps,
-                                             tw_dtype dtype, unsigned flags, tw_rows_sink sink, void* sink_ctx,
-                                             const int64_t* rows_consumed, int n_consumed) {
+tw_status tw_rmsnorm_residual_host_sync_gated(const void* h_input, const void* h_residual, void* h_residual_out,
+                                              void* h_output, const float* h_weight, int64_t T, int64_t H,
+                                              float eps, tw_dtype dtype, unsigned flags, const int64_t* rows_ready,
+                                              int n_ready) {
   clear_error();
-  if (sink && (n_consumed < 1 || !rows_consumed))
-    return fail(TW_ERR_DIMENSION, "rmsnorm_residual_host_sync: a sink needs rows_consumed counters");
+  if (n_ready < 0 || (n_ready > 0 && !rows_ready))
+    return fail(TW_ERR_DIMENSION, "rmsnorm_residual_host_sync: bad rows_ready gate");
   if (T < 0 || H < 1) return fail(TW_ERR_DIMENSION, "rmsnorm_residual_host_sync: requires T >= 0 and H >= 1");
   if (!(eps > 0.0f) && eps != 0.0f)
     return fail(TW_ERR_NUMERIC, "rmsnorm_residual_host_sync: epsilon must be nonnegative");
   if (dtype != TW_BF16 && dtype != TW_F32) return fail(TW_ERR_CONFIG, "rmsnorm_residual_host_sync: unknown dtype");
   if (T == 0) return TW_OK;
-  if (!h_input || !h_residual || !h_weight || (!sink && (!h_residual_out || !h_output)))
+  if (!h_input || !h_residual || !h_residual_out || !h_output || !h_weight)
     return fail(TW_ERR_DIMENSION, "rmsnorm_residual_host_sync: null buffer");
   const bool bf16 = dtype == TW_BF16;
   const bool check = flags & TW_HOST_CHECK_FINITE;
@@ -374,7 +351,6 @@ tw_status tw_rmsnorm_residual_host_sync_sink(const void* h_input, const void* h_
   const size_t cb = static_cast<size_t>(chunk_rows) * row;
   tw_status st = ensure(c, dev, cb, static_cast<size_t>(H) * sizeof(float));
   if (st == TW_OK) st = ensure_ring(g, dev, cb);
-  if (st == TW_OK && sink) st = ensure_out_windows(g, cb);
   if (st != TW_OK) return st;
   cudaError_t e = cudaSuccess;
   for (cudaStream_t s : {c.h2d, c.comp, c.d2h}) cudaStreamWaitEvent(s, c.done, 0);
@@ -414,23 +390,19 @@ tw_status tw_rmsnorm_residual_host_sync_sink(const void* h_input, const void* h_
     });
     return bad.load();
   };
-  // every consumer counter at or past `rows` (sink mode)
-  auto wait_consumed = [&](int64_t rows) {
-    for (int i = 0; i < n_consumed; ++i)
-      for (int spins = 0; __atomic_load_n(rows_consumed + i, __ATOMIC_ACQUIRE) < rows; ++spins)
-        if (spins < 4096) cpu_relax(); else std::this_thread::yield();
-  };
   auto copy_out = [&](int64_t k) -> tw_status {
     const int s = static_cast<int>(k % kSlots);
     cudaError_t ee = cudaEventSynchronize(g.drained[s]);
     if (ee != cudaSuccess) return drain(cuda_fail(ee, "host_sync: D2H"));
     size_t off, nb;
     span(k, &off, &nb);
-    if (sink) {
-      const int o = static_cast<int>(k % kOutSlots);
-      sink(sink_ctx, k * chunk_rows, static_cast<int64_t>(nb / row), g.ho[o][0], g.ho[o][1]);
-      return TW_OK;
-    }
+    // the caller may still be preparing the destination rows (the drop-in
+    // value-initialises its result vectors on helper threads): wait until
+    // every gate covers this chunk
+    const int64_t need = std::min(T, (k + 1) * chunk_rows);
+    for (int i = 0; i < n_ready; ++i)
+      for (int spins = 0; __atomic_load_n(rows_ready + i, __ATOMIC_ACQUIRE) < need; ++spins)
+        if (spins < 4096) cpu_relax(); else std::this_thread::yield();
     pcopy(hout + off, static_cast<const char*>(g.h[s][2]), hro + off, static_cast<const char*>(g.h[s][3]), nb,
           false);
     return TW_OK;
@@ -457,23 +429,14 @@ tw_status tw_rmsnorm_residual_host_sync_sink(const void* h_input, const void* h_
     if (st != TW_OK) return drain(st);
     cudaEventRecord(c.computed[s], c.comp);
     cudaStreamWaitEvent(c.d2h, c.computed[s], 0);
-    void* dout = g.h[s][2];
-    void* dres = g.h[s][3];
-    if (sink) {  // window k % kOutSlots, once the caller has consumed chunk k - kOutSlots from it
-      const int o = static_cast<int>(k % kOutSlots);
-      if (k >= kOutSlots) wait_consumed((k - kOutSlots + 1) * chunk_rows);
-      dout = g.ho[o][0];
-      dres = g.ho[o][1];
-    }
-    if ((e = cudaMemcpyAsync(dout, b[2], nb, cudaMemcpyDeviceToHost, c.d2h)) != cudaSuccess ||
-        (e = cudaMemcpyAsync(dres, b[3], nb, cudaMemcpyDeviceToHost, c.d2h)) != cudaSuccess)
+    if ((e = cudaMemcpyAsync(g.h[s][2], b[2], nb, cudaMemcpyDeviceToHost, c.d2h)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(g.h[s][3], b[3], nb, cudaMemcpyDeviceToHost, c.d2h)) != cudaSuccess)
       return drain(cuda_fail(e, "host_sync: D2H"));
     cudaEventRecord(g.drained[s], c.d2h);
   }
   if (nonfinite) return drain(fail(TW_ERR_NUMERIC, "TokenMatrix contains NaN/Inf"));
   for (int64_t k = std::max<int64_t>(0, K - kSlots); k < K; ++k)
     if ((st = copy_out(k)) != TW_OK) return drain(st);
-  if (sink) wait_consumed(T);  // the windows are free for the next call
   cudaEventRecord(c.done, c.d2h);  // every chunk drained (copy_out synchronised on each)
   return TW_OK;
 }

@@ -8,7 +8,6 @@
 // There is no CPU compute fallback: without a GPU these throw DeviceError.
 #include <algorithm>
 #include <atomic>
-#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -26,31 +25,9 @@ namespace weavesim {
 
 namespace {
 
-// result matrices at least this large are built by appender threads from the
-// pipeline's result windows (rmsnorm_residual below)
+// result matrices at least this large are value-initialised on helper threads
+// overlapped with the transfers (rmsnorm_residual below)
 constexpr size_t kOverlapFillBytes = 16u << 20;
-
-// Chunk descriptors from tw_rmsnorm_residual_host_sync_sink to the two
-// appender threads of rmsnorm_residual: single producer (the pipeline's
-// calling thread), two consumers; the pipeline keeps at most kOutSlots
-// chunks unconsumed, far below kDepth.
-struct RowsSink {
-  static constexpr int kDepth = 64;
-  struct Chunk {
-    std::int64_t row0, rows;
-    const float* output;
-    const float* residual_out;
-  };
-  Chunk ring[kDepth];
-  std::atomic<std::int64_t> published{0};
-  std::atomic<bool> stop{false};
-  static void on_rows(void* ctx, std::int64_t row0, std::int64_t rows, const void* out, const void* res) {
-    auto* q = static_cast<RowsSink*>(ctx);
-    const std::int64_t k = q->published.load(std::memory_order_relaxed);
-    q->ring[k % kDepth] = {row0, rows, static_cast<const float*>(out), static_cast<const float*>(res)};
-    q->published.store(k + 1, std::memory_order_release);
-  }
-};
 
 [[noreturn]] void throw_status(tw_status st, const std::string& where) {
   const std::string msg = where + ": " + tw_last_error();
@@ -226,43 +203,41 @@ NormResult rmsnorm_residual(const TokenMatrix& input, const TokenMatrix& residua
   // The two fresh result matrices (TokenMatrix::zeros in the reference) are
   // allocated here, on the calling thread -- a second thread would allocate
   // from its own glibc arena, measured 5x slower for 256 MiB blocks -- and
-  // built by two appender threads directly from the pipeline's pinned result
-  // windows, chunk by chunk in row order (insert within the reserved capacity:
-  // no reallocation, no zero-fill; the zero-fill alone was 2 x ~18 ms of
-  // single-thread work at 8192 x 8192, and the copy-out another pass).
+  // value-initialised by two helper threads in ~4 MiB steps while the
+  // pipeline stages, transfers and computes (2 x ~18 ms of single-thread
+  // zero-fill at 8192 x 8192 that used to precede it).  resize() within the
+  // reserved capacity never reallocates, so the row pointers taken below
+  // stay valid; the pipeline copies chunk k's results in only once both
+  // fills have published rows past it (tw_rmsnorm_residual_host_sync_gated).
   for (TokenMatrix* m : {&result.output, &result.residual_out}) {
     m->num_tokens = T;
     m->hidden = H;
     m->values.reserve(n);
   }
-  RowsSink q;
-  alignas(64) std::int64_t consumed[2] = {0, 0};
-  auto append = [&](std::vector<float>* v, int which) {
-    for (std::int64_t j = 0;; ++j) {
-      for (int spins = 0; q.published.load(std::memory_order_acquire) <= j; ++spins) {
-        if (q.stop.load(std::memory_order_relaxed)) return;
-        if (spins < 4096) std::this_thread::yield();
-        else std::this_thread::sleep_for(std::chrono::microseconds(20));
-      }
-      const RowsSink::Chunk& c = q.ring[j % RowsSink::kDepth];
-      const float* src = which ? c.residual_out : c.output;
-      v->insert(v->end(), src, src + c.rows * H);
-      __atomic_store_n(&consumed[which], c.row0 + c.rows, __ATOMIC_RELEASE);
-      if (c.row0 + c.rows >= T) return;
+  float* out = result.output.values.data();
+  float* res_out = result.residual_out.values.data();
+  alignas(64) std::int64_t ready[2] = {0, 0};
+  std::atomic<bool> stop{false};
+  const std::int64_t step = std::max<std::int64_t>(1, static_cast<std::int64_t>((4u << 20) / (H * sizeof(float))));
+  auto fill = [&](std::vector<float>* v, std::int64_t* rows) {
+    for (std::int64_t t = 0; t < T && !stop.load(std::memory_order_relaxed);) {
+      t = std::min(T, t + step);
+      v->resize(static_cast<size_t>(t * H));
+      __atomic_store_n(rows, t, __ATOMIC_RELEASE);
     }
   };
-  std::thread a0(append, &result.output.values, 0);
-  std::thread a1(append, &result.residual_out.values, 1);
+  std::thread f0(fill, &result.output.values, &ready[0]);
+  std::thread f1(fill, &result.residual_out.values, &ready[1]);
   tw_status st;
   {
     std::lock_guard<std::mutex> lock(g_mu);
-    st = tw_rmsnorm_residual_host_sync_sink(input.values.data(), residual.values.data(), nullptr, nullptr,
-                                            params.weight.data(), T, H, params.epsilon, TW_F32, TW_HOST_CHECK_FINITE,
-                                            &RowsSink::on_rows, &q, consumed, 2);
+    st = tw_rmsnorm_residual_host_sync_gated(input.values.data(), residual.values.data(), res_out, out,
+                                             params.weight.data(), T, H, params.epsilon, TW_F32,
+                                             TW_HOST_CHECK_FINITE, ready, 2);
   }
-  if (st != TW_OK) q.stop.store(true, std::memory_order_relaxed);
-  a0.join();
-  a1.join();
+  if (st != TW_OK) stop.store(true, std::memory_order_relaxed);
+  f0.join();
+  f1.join();
   if (st == TW_ERR_NUMERIC) throw NumericError("TokenMatrix contains NaN/Inf");
   check(st, "rmsnorm_residual");
   return result;
