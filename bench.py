@@ -580,8 +580,10 @@ def main():
     ap.add_argument("--hidden", type=int, default=8192)
     ap.add_argument("--sm-budget", type=int, default=8, help="K1 CTAs (= SMs) per rank (N>1)")
     ap.add_argument("--gather-residual", action="store_true", help="K1 G=2 (N>1)")
-    ap.add_argument("--transport", choices=["nvls", "peer", "auto"], default="nvls",
-                    help="N>1 on distinct GPUs: nvls (default; fail if unavailable), peer, or auto")
+    ap.add_argument("--transport", choices=["nvls", "peer", "auto"], default="auto",
+                    help="N>1 on distinct GPUs: auto (default: NVLS, or PEER over NVLink with the line labelled "
+                         "and a stderr warning when the multicast object cannot be built), nvls (fail if "
+                         "unavailable) or peer")
     ap.add_argument("--quick", action="store_true", help="skip sweeps/baselines (profiling runs)")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -76,6 +76,17 @@ def test_nvlink_roofline_bytes():
     assert abs(algorithmic_nvlink_bytes(8192, 8192, 8, True) / 1e6 - 285.21) < 0.01
 
 
+def test_peer_roofline_bytes():
+    """The labelled PEER fallback's bytes: (N-1)/N of every peer's partial in,
+    G*(N-1)/N of the output (and r') out, per direction."""
+    from tools.bench_tp import alg_bytes, algorithmic_nvlink_bytes, algorithmic_peer_bytes
+    S = 8192 * 8192 * 2
+    assert algorithmic_peer_bytes(8192, 8192, 8, False) == S * 2 * 7 / 8
+    assert algorithmic_peer_bytes(8192, 8192, 2, True) == S * 3 / 2
+    assert alg_bytes("peer", 1024, 8192, 4, False) == algorithmic_peer_bytes(1024, 8192, 4, False)
+    assert alg_bytes("nvls", 1024, 8192, 4, True) == algorithmic_nvlink_bytes(1024, 8192, 4, True)
+
+
 def test_nvlink_counter_parse():
     from tools.bench_tp import parse_nvlink_counters
     text = """GPU 0: NVIDIA B200 (UUID: GPU-x)

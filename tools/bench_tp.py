@@ -3,9 +3,13 @@ AllReduce + residual-add + RMSNorm) over the multi-process communicator
 (tw_comm_create_mp), strong scaling at the same T.
 
 Transport.  Ranks on distinct GPUs run the NVLS kernel (multimem ld_reduce /
-st over an NVSwitch multicast object) and nothing else: if the multicast
-object cannot be built the run FAILS instead of falling back to PEER, so a
-printed TP line is always an NVLS number.  Ranks sharing one GPU (the
+st over an NVSwitch multicast object).  If the multicast object cannot be
+built (no NVSwitch multicast in the box or container), the default `auto`
+falls back collectively to K1's PEER engine over NVLink P2P -- still a
+multi-GPU NVLink measurement of the fused kernel, but not the NVLS one -- and
+says so: a warning on stderr, `config.transport` = "peer", a top-level
+`nvls_unavailable` key and PEER's algorithmic bytes in the roofline.
+`--transport nvls` fails instead.  Ranks sharing one GPU (the
 two-process test topology of a one-GPU box) cannot bind a multicast object;
 they run PEER and the line says "colocated": such numbers are plumbing checks,
 not NVLink measurements.
@@ -27,6 +31,7 @@ import os
 import re
 import statistics
 import subprocess
+import sys
 import time
 import uuid
 
@@ -56,6 +61,21 @@ def algorithmic_nvlink_bytes(T: int, H: int, world: int, gather_residual: bool, 
     S = T * H * elem
     G = 2 if gather_residual else 1
     return S * (G + 1.0 / world)
+
+
+def algorithmic_peer_bytes(T: int, H: int, world: int, gather_residual: bool, elem: int = 2) -> float:
+    """Per GPU per direction, PEER (P2P loads/stores over NVLink): B = S*(1+G)*(N-1)/N.
+    Ingress: this rank's shard of every peer's partial, (N-1)*S/N; egress:
+    G*(N-1)*S/N of normed output (and r') stored into every peer."""
+    S = T * H * elem
+    G = 2 if gather_residual else 1
+    return S * (1 + G) * (world - 1) / world
+
+
+def alg_bytes(transport: str, T: int, H: int, world: int, gather_residual: bool) -> float:
+    if transport == "nvls":
+        return algorithmic_nvlink_bytes(T, H, world, gather_residual)
+    return algorithmic_peer_bytes(T, H, world, gather_residual)
 
 
 def nvlink_counters(device_index: int):
@@ -130,6 +150,13 @@ class _Rank:
         wsz, tr, nb = ctypes.c_int(), ctypes.c_int(), ctypes.c_size_t()
         _lib.check(_lib.lib.tw_comm_info(h, ctypes.byref(wsz), ctypes.byref(tr), ctypes.byref(nb)))
         self.transport = _lib.TRANSPORT_NAMES[tr.value]
+        self.nvls_unavailable = None
+        if not self.colocated and self.transport != "nvls":
+            self.nvls_unavailable = (f"transport {tname}: the NVLS multicast object was not available on this box; "
+                                     f"K1 ran its PEER engine over NVLink P2P")
+            if self.rank == 0:
+                print(f"WARNING: {self.nvls_unavailable} -- the TP line is a PEER number, not NVLS",
+                      file=sys.stderr, flush=True)
         self.stream = torch.cuda.Stream()
         self.tiny = torch.zeros(1, device="cuda")
 
@@ -254,7 +281,7 @@ def run_tp(args):
             ts = R.timed(lambda: R.fused(T, residual, weight, bud, gather), 10, flush)
             u = R.max_mean_us(ts)
             sweep_b[str(bud)] = {"us": round(u, 2),
-                                 "nvlink_gbs": round(algorithmic_nvlink_bytes(T, H, world, gather) / u / 1e3, 1)}
+                                 "nvlink_gbs": round(alg_bytes(R.transport, T, H, world, gather) / u / 1e3, 1)}
         extra["sm_budget_sweep"] = sweep_b
         sweep_t = {}
         for t in (256, 1024, 2048, 4096, 8192):
@@ -263,7 +290,7 @@ def run_tp(args):
             ts = R.timed(lambda: R.fused(t, residual, weight, budget, gather), 10, flush)
             u = R.max_mean_us(ts)
             sweep_t[str(t)] = {"us": round(u, 2),
-                               "nvlink_gbs": round(algorithmic_nvlink_bytes(t, H, world, gather) / u / 1e3, 1)}
+                               "nvlink_gbs": round(alg_bytes(R.transport, t, H, world, gather) / u / 1e3, 1)}
         extra["token_sweep"] = sweep_t
         ts = R.timed(lambda: R.fused(T, residual, weight, budget, True), 10, flush)
         extra["gather_residual_G2_us"] = round(R.max_mean_us(ts), 2)
@@ -314,7 +341,8 @@ def run_tp(args):
         cpu = cpu_baseline_fused(world, T, H)
     R.dist.barrier()
 
-    alg = algorithmic_nvlink_bytes(T, H, world, gather)
+    alg = alg_bytes(R.transport, T, H, world, gather)
+    alg_formula = "S*(G+1/N), S = T*H*2 (NVLS)" if R.transport == "nvls" else "S*(1+G)*(N-1)/N, S = T*H*2 (PEER)"
     achieved = alg / (us * 1e-6) / 1e9
     traffic = None
     if nvl0 and nvl1:
@@ -339,7 +367,7 @@ def run_tp(args):
                          "achieved": round(achieved, 1), "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
                          "frac": round(achieved / NVLINK_PEAK_GBS, 4),
                          "peak_kind": "nominal NVLink 5 per direction per GPU",
-                         "alg_bytes_per_launch": alg, "alg_bytes_formula": "S*(G+1/N), S = T*H*2",
+                         "alg_bytes_per_launch": alg, "alg_bytes_formula": alg_formula,
                          "traffic": traffic},
             "kernel_us": {"mean": round(us, 3), "median": round(us_med, 3)},
             "sms_consumed": budget,
@@ -352,6 +380,8 @@ def run_tp(args):
             "clocks": clk.summary() if clk else None,
             "cpu_baseline": cpu,
         }
+        if R.nvls_unavailable:
+            line["nvls_unavailable"] = R.nvls_unavailable
         if R.colocated:
             line["note"] = ("ranks share one GPU: PEER transport, time-sliced -- a plumbing check, "
                             "not an NVLink measurement")
