@@ -128,3 +128,24 @@ def test_staged_copies_validate_on_the_host():
     assert L.tw_memcpy_d2h_staged(p, None, 16) == _lib.TW_ERR_DIMENSION
     assert L.tw_memcpy_d2h_staged(p, p, 16) == _lib.TW_ERR_CONFIG
     assert L.tw_memcpy_d2h_staged(p, p, 0) == _lib.TW_OK
+
+
+def test_gated_host_sync_validates_on_the_host():
+    """tw_rmsnorm_residual_host_sync_gated (the drop-in's overlapped-fill
+    path) rejects a malformed gate before anything else, then validates like
+    tw_rmsnorm_residual_host_sync; T == 0 is a no-op."""
+    import ctypes
+    from paper_2505_11329_b200 import _lib
+    L = _lib.lib
+    ready = (ctypes.c_int64 * 2)(0, 0)
+    assert L.tw_rmsnorm_residual_host_sync_gated(None, None, None, None, None, 4, 8, 1e-5, _lib.TW_F32, 0,
+                                                  None, 2) == _lib.TW_ERR_DIMENSION
+    assert b"gate" in L.tw_last_error()
+    assert L.tw_rmsnorm_residual_host_sync_gated(None, None, None, None, None, 4, 8, 1e-5, _lib.TW_F32, 0,
+                                                  ready, -1) == _lib.TW_ERR_DIMENSION
+    assert L.tw_rmsnorm_residual_host_sync_gated(None, None, None, None, None, 4, 8, -1.0, _lib.TW_F32, 0,
+                                                  ready, 2) == _lib.TW_ERR_NUMERIC
+    assert L.tw_rmsnorm_residual_host_sync_gated(None, None, None, None, None, 4, 8, 1e-5, _lib.TW_F32, 0,
+                                                  ready, 2) == _lib.TW_ERR_DIMENSION  # null buffers
+    assert L.tw_rmsnorm_residual_host_sync_gated(None, None, None, None, None, 0, 8, 1e-5, _lib.TW_F32, 0,
+                                                  ready, 2) == _lib.TW_OK
