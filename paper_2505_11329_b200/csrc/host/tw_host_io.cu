@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -223,9 +224,18 @@ class HostPool {
   static constexpr int kCallerSpins = 1 << 16;
   static constexpr std::chrono::microseconds kIdleSpin{500};
   HostPool() {
-    // every hardware thread (the caller is one of them): the staging copies
-    // are host-memory-bandwidth work and the caller blocks on them
-    const unsigned hw = std::max(2u, std::thread::hardware_concurrency());
+    // Half the hardware threads (the caller is one of them): the staging
+    // copies are host-memory-bandwidth work that saturates well before every
+    // core copies, and the spare cores keep the caller's other threads (the
+    // drop-in's result fills, the CUDA driver's) off the pool's cores.  On the
+    // 16-vCPU B200 VMs, interleaved A/B (profiles/dropin_fill_ab_r02.txt):
+    // the drop-in rmsnorm_residual 40-43 ms with 16 threads, 30.6-31.4 with 8;
+    // the TP = 2 fused op 8.7-9.0 vs 8.2-8.4 ms.  TW_HOST_THREADS overrides.
+    unsigned hw = std::max(2u, std::thread::hardware_concurrency() / 2);
+    if (const char* e = std::getenv("TW_HOST_THREADS")) {
+      const int v = std::atoi(e);
+      if (v >= 1) hw = static_cast<unsigned>(v);
+    }
     const int workers = static_cast<int>(std::min(32u, hw)) - 1;
     for (int i = 0; i < std::max(0, workers); ++i)
       threads_.emplace_back([this] { loop(); });
