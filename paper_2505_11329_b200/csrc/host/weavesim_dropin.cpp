@@ -29,6 +29,33 @@ namespace {
 // overlapped with the transfers (rmsnorm_residual below)
 constexpr size_t kOverlapFillBytes = 16u << 20;
 
+// A fresh result matrix (TokenMatrix::zeros in the reference) whose
+// value-initialisation runs on a helper thread while the caller stages the
+// inputs and the kernels run; wait() before the results are copied in.  The
+// storage is allocated on the calling thread (glibc's main arena).
+class ZerosBehind {
+ public:
+  ZerosBehind(TokenMatrix& m, std::int64_t T, std::int64_t H) : m_(m) {
+    const size_t n = static_cast<size_t>(T * H);
+    m.num_tokens = T;
+    m.hidden = H;
+    if (n * sizeof(float) < kOverlapFillBytes) {
+      m.values.assign(n, 0.0f);
+      return;
+    }
+    m.values.reserve(n);
+    t_ = std::thread([this, n] { m_.values.resize(n); });
+  }
+  void wait() {
+    if (t_.joinable()) t_.join();
+  }
+  ~ZerosBehind() { wait(); }  // exception paths: never leave the thread running
+
+ private:
+  TokenMatrix& m_;
+  std::thread t_;
+};
+
 [[noreturn]] void throw_status(tw_status st, const std::string& where) {
   const std::string msg = where + ": " + tw_last_error();
   switch (st) {
@@ -362,11 +389,14 @@ void* chain_sum_on_device(const RankGroup& group) {
 // (the caller has checked everything else, in the reference's order).
 TokenMatrix reduce_on_device(const RankGroup& group, bool scan = false) {
   const std::int64_t T = group.num_tokens(), H = group.hidden();
-  TokenMatrix out = TokenMatrix::zeros(T, H);
-  if (T == 0) return out;
+  TokenMatrix out;
+  if (T == 0) return TokenMatrix::zeros(T, H);
+  ZerosBehind zeros(out, T, H);
   const size_t nb = static_cast<size_t>(T * H) * sizeof(float);
   if (group.world_size > TW_MAX_RANKS) {
-    d2h(out.values.data(), chain_sum_on_device(group), nb, "D2H all_reduce");
+    void* sum = chain_sum_on_device(group);
+    zeros.wait();
+    d2h(out.values.data(), sum, nb, "D2H all_reduce");
     return out;
   }
   GroupContext& ctx = context_for(group.world_size, nb);
@@ -376,6 +406,7 @@ TokenMatrix reduce_on_device(const RankGroup& group, bool scan = false) {
   check(tw_comm_check(ctx.comm), "all_reduce");
   void* src = nullptr;
   check(tw_comm_buffer(ctx.comm, 0, TW_BUF_OUTPUT, &src), "comm_buffer");
+  zeros.wait();
   d2h(out.values.data(), src, nb, "D2H all_reduce");
   return out;
 }
@@ -463,10 +494,11 @@ TokenMatrix fused_allreduce_rmsnorm(RankGroup& group, const NormParams& params, 
       throw DimensionError("fused_allreduce_rmsnorm: weight length must equal hidden size");
   }
   const std::int64_t T = group.num_tokens(), H = group.hidden();
-  TokenMatrix output = TokenMatrix::zeros(T, H);
-  if (T == 0) return output;
+  if (T == 0) return TokenMatrix::zeros(T, H);
   const int W = group.world_size;
   const size_t nb = static_cast<size_t>(T * H) * sizeof(float);
+  TokenMatrix output;
+  ZerosBehind zeros(output, T, H);
   std::lock_guard<std::mutex> lock(g_mu);
   if (W > TW_MAX_RANKS) {
     // wider than a communicator: the chained rank-order sum, then one K2 over
@@ -485,6 +517,7 @@ TokenMatrix fused_allreduce_rmsnorm(RankGroup& group, const NormParams& params, 
                               params.epsilon, TW_F32, 0, nullptr),
           "fused_allreduce_rmsnorm");
     check(tw_device_synchronize(0), "fused_allreduce_rmsnorm");
+    zeros.wait();
     d2h(output.values.data(), w.out.ptr, nb, "D2H output");
     d2h(res.data(), w.tmp.ptr, nb, "D2H residual");
     for (int r = 0; r < W; ++r)
@@ -516,6 +549,7 @@ TokenMatrix fused_allreduce_rmsnorm(RankGroup& group, const NormParams& params, 
   check(tw_comm_check(ctx.comm), "fused_allreduce_rmsnorm");
   void* src = nullptr;
   check(tw_comm_buffer(ctx.comm, 0, TW_BUF_OUTPUT, &src), "comm_buffer");
+  zeros.wait();
   d2h(output.values.data(), src, nb, "D2H output");
   for (int r = 0; r < W; ++r) {
     const size_t rb = group.residual_shards[r].values.size() * sizeof(float);
