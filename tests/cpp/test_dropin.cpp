@@ -10,6 +10,7 @@
 #include <chrono>
 #include <fstream>
 #include <cmath>
+#include <tuple>
 #include <cstdio>
 #include <cstring>
 #include <random>
@@ -227,12 +228,17 @@ void gpu_cases() {
   }
   // test_collectives.cpp:94-114 -- fused vs unfused composition
   // worlds above TW_MAX_RANKS take the drop-in's chained path (the reference
-  // accepts any N >= 2)
-  for (int world : {2, 4, 8, 12, 16}) {
-    for (std::int64_t tokens : {1, 3, 17, 40}) {
-      RankGroup group = random_group(world, tokens, 32, 77 * world + tokens);
+  // accepts any N >= 2); 1027 x 4096 (16 MiB outputs) takes the helper-thread
+  // output fill in all_reduce, reduce_scatter and fused_allreduce_rmsnorm
+  for (auto [world, tokens, hidden] : {std::tuple<int, std::int64_t, std::int64_t>{2, 1, 32}, {2, 3, 32},
+                                       {2, 17, 32}, {2, 40, 32}, {4, 1, 32}, {4, 3, 32}, {4, 17, 32}, {4, 40, 32},
+                                       {8, 1, 32}, {8, 3, 32}, {8, 17, 32}, {8, 40, 32}, {12, 1, 32}, {12, 3, 32},
+                                       {12, 17, 32}, {12, 40, 32}, {16, 1, 32}, {16, 3, 32}, {16, 17, 32},
+                                       {16, 40, 32}, {2, 1027, 4096}, {3, 1027, 4096}, {12, 1027, 4096}}) {
+    {
+      RankGroup group = random_group(world, tokens, hidden, 77 * world + tokens);
       const ShardMap shards = token_shard_map(tokens, world);
-      const NormParams params = unit_norm(32);
+      const NormParams params = unit_norm(hidden);
       const TokenMatrix reduced = all_reduce(group);
       const TokenMatrix residual = all_gather(group.residual_shards, shards);
       const NormResult oracle = rmsnorm_residual(reduced, residual, params);
@@ -242,6 +248,16 @@ void gpu_cases() {
         ok = std::abs(fused.values[i] - oracle.output.values[i]) <= 1e-5;
       CHECK(ok);
       CHECK(all_gather(group.residual_shards, shards).values == oracle.residual_out.values);
+      if (hidden == 4096) {  // the large outputs: rank-ascending fp32 sum, RS o AG == AR, bitwise
+        bool exact = true;
+        for (size_t i = 0; exact && i < reduced.values.size(); ++i) {
+          float e = 0.0f;
+          for (const TokenMatrix& m : group.inputs) e += m.values[i];
+          exact = reduced.values[i] == e;
+        }
+        CHECK(exact);
+        CHECK(all_gather(reduce_scatter(group, shards), shards).values == reduced.values);
+      }
     }
   }
   // test_collectives.cpp:116-127 -- parallel flag is bitwise neutral
