@@ -207,6 +207,62 @@ def test_k2_host_sync_pageable(cuda, orc, T, H, dtype_name):
                                                    tw.TW_BF16 if bf else tw.TW_F32, 0))
 
 
+@pytest.mark.parametrize("dtype_name", ["float32", "bfloat16"])
+@pytest.mark.parametrize("T,H", [(37, 33), (1100, 8192)])
+def test_k2_host_sync_gated(cuda, orc, T, H, dtype_name):
+    """tw_rmsnorm_residual_host_sync_gated: two row gates advanced by a host
+    thread in small uneven steps (as the drop-in's fill threads do) -- the
+    results land only behind the gates and equal the oracle's; gates already
+    at T behave like the ungated call."""
+    import ctypes
+    import threading
+    import time
+    import paper_2505_11329_b200 as tw
+    from paper_2505_11329_b200 import _lib
+    inp, res, w = norm_inputs(5 * T + H, T, H)
+    bf = dtype_name == "bfloat16"
+    if bf:
+        inp, res = bf16_round(inp), bf16_round(res)
+        hi = (inp.view(np.uint32) >> 16).astype(np.uint16)
+        hr = (res.view(np.uint32) >> 16).astype(np.uint16)
+    else:
+        hi, hr = np.ascontiguousarray(inp), np.ascontiguousarray(res)
+    want_out, want_res = orc.rmsnorm_residual(inp, res, w)
+    p = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    code = tw.TW_BF16 if bf else tw.TW_F32
+    for threaded in (True, False):
+        ho, hro = np.zeros_like(hi), np.zeros_like(hi)
+        gates = (ctypes.c_int64 * 2)(0, 0) if threaded else (ctypes.c_int64 * 2)(T, T)
+        seen = []
+
+        def advance():
+            for t in list(range(0, T, max(1, T // 7))) + [T]:
+                seen.append(int(np.count_nonzero(hro.reshape(T, -1).any(axis=1))))  # rows written so far
+                gates[0] = t
+                time.sleep(0.002)
+                gates[1] = t
+                time.sleep(0.002)
+
+        th = threading.Thread(target=advance) if threaded else None
+        if th:
+            th.start()
+        tw.check(_lib.lib.tw_rmsnorm_residual_host_sync_gated(p(hi), p(hr), p(hro), p(ho), p(w), T, H, 1e-5, code,
+                                                              _lib.TW_HOST_CHECK_FINITE, gates, 2))
+        if th:
+            th.join()
+            steps = list(range(0, T, max(1, T // 7)))
+            # before gate step k was published, no row at or beyond step k-1's value had been written
+            for k, rows in enumerate(seen[1:], start=1):
+                assert rows <= steps[k - 1] if k - 1 < len(steps) else True, (k, rows)
+        if bf:
+            up = lambda a: (a.astype(np.uint32) << 16).view(np.float32)  # noqa: E731
+            assert np.array_equal(up(hro), bf16_round(want_res))
+            assert_bf16_close(up(ho), want_out)
+        else:
+            assert np.array_equal(hro, want_res)
+            assert_abs_close(ho, want_out, 1e-5)
+
+
 @pytest.mark.parametrize("engine,pipeline,groups,lookahead",
                          [("rows", "1", "1", "0"), ("rows", "0", "1", "0"), ("bulk", "0", "1", "0"),
                           ("tma", "0", "1", "0"), ("tma", "0", "2", "0"), ("flat", "0", "1", "0"),
