@@ -14,6 +14,9 @@ two-process test topology of a one-GPU box) cannot bind a multicast object;
 they run PEER and the line says "colocated": such numbers are plumbing checks,
 not NVLink measurements.
 
+Parity.  Before timing, one K1 launch on the line's own inputs is checked
+against a torch fp32 restatement on every rank (`parity` in the line).
+
 Timing.  Each step: L2 flush on the rank's stream (a 256 MiB write + read,
 outside the events), a device-side cross-rank sync (a one-element NCCL
 all_reduce on the same stream, so every rank's K1 starts within the
@@ -232,7 +235,11 @@ def run_tp(args):
     inp = R.buffer(_lib.TW_BUF_INPUT, T)
     inp.copy_((torch.rand(T, H, device="cuda", generator=g) - 0.5).to(torch.bfloat16))
     residual = (torch.rand(max(e - b, 1), H, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
-    weight = torch.rand(H, device="cuda", generator=g) + 0.5
+    # the RMSNorm weight is replicated (as a TP model's is): the same draw on every rank
+    weight = torch.rand(H, device="cuda", generator=torch.Generator(device="cuda").manual_seed(1 << 20)) + 0.5
+
+    # ---- parity first: one K1 call against a torch fp32 restatement ----
+    parity = check_parity(R, inp, residual, weight, T, budget, gather)
 
     # ---- the headline: K1 at T, `budget` SMs, per-step events ----
     clk = ClockSampler(R.local) if rank == 0 else None
@@ -380,6 +387,7 @@ def run_tp(args):
             "clocks": clk.summary() if clk else None,
             "cpu_baseline": cpu,
         }
+        line["parity"] = parity
         if R.nvls_unavailable:
             line["nvls_unavailable"] = R.nvls_unavailable
         if R.colocated:
@@ -389,6 +397,49 @@ def run_tp(args):
         print(json.dumps(line), flush=True)
     R.close()
     return 0
+
+
+def check_parity(R, inp, residual, weight, T, budget, gather):
+    """One K1 launch on the line's own inputs against a torch fp32
+    restatement of fused_allreduce_rmsnorm (proj/src/collectives.cpp:134-153):
+    v = sum over ranks of the bf16 partials (a torch.distributed all_reduce
+    in fp32: the checker, not the measured path), r' = v + residual,
+    out = r' * rsqrt(mean(r'^2) + eps) * w.  bf16 bar as the tests': |err| <=
+    2e-2 * |want| + 2e-2 (the hardware reduction order is not fixed and v is
+    rounded to bf16 before the add).  Checks the replicated output on every
+    rank and the rank's own r' rows; restores the residual afterwards."""
+    torch = R.torch
+    b, e = R.tw.token_shard_map(T, R.world)[R.rank]
+    res0 = residual.clone()
+    R.sync()
+    R.fused(T, residual, weight, budget, gather)
+    torch.cuda.synchronize()
+    R._lib.check(R._lib.lib.tw_comm_check(R.h))
+    out = R.buffer(R._lib.TW_BUF_OUTPUT, T).float()
+    dev = "cuda" if R.red_device == "cuda" else "cpu"
+    v = inp.float().to(dev)
+    R.dist.all_reduce(v)
+    full_res = torch.zeros(T, R.H, dtype=torch.float32, device=dev)
+    if e > b:
+        full_res[b:e] = res0[: e - b].float().to(dev)
+    R.dist.all_reduce(full_res)
+    r = (v + full_res).to(out.device)
+    want = r * torch.rsqrt(r.pow(2).mean(dim=1, keepdim=True) + EPS) * weight.float()
+
+    def excess(got, ref):  # > 0 where the bf16 bar is broken
+        return float(((got - ref).abs() - (2e-2 * ref.abs() + 2e-2)).max()) if got.numel() else -1.0
+
+    worst_out = excess(out, want)
+    worst_res = excess(residual[: e - b].float(), r[b:e]) if e > b else -1.0
+    max_abs = float((out - want).abs().max())
+    residual.copy_(res0)
+    torch.cuda.synchronize()
+    worst = max_over_ranks(max(worst_out, worst_res), R.dist, R.red_device)
+    max_abs = max_over_ranks(max_abs, R.dist, R.red_device)
+    return {"ok": worst <= 0.0, "max_abs_err_output": round(max_abs, 5),
+            "bar": "|err| <= 2e-2*|want| + 2e-2 (bf16), output on every rank and each rank's r' rows",
+            "checker": "torch fp32 restatement; partials summed by a torch.distributed all_reduce (not timed)",
+            "T": T, "gather_residual": gather}
 
 
 def cpu_baseline_fused(world, T, H, iters=3):
