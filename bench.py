@@ -296,13 +296,52 @@ def k2_e2e(T, H, bufs, steps, dtype=None):
     torch.cuda.synchronize()
     per = sorted(1e3 * ev[i].elapsed_time(ev[i + 1]) for i in range(steps))
     nb = T * H * hx.element_size()
+    # the host results of the last step, checked (outside the clock)
+    if dt == torch.bfloat16:  # vs the device K2 (itself checked by k2_parity): r' bitwise, out at the bf16 bar
+        _, _, _, out, rout = bufs
+        d = (ho.cuda().float() - out.float()).abs()
+        worst = float((d - (2e-2 * out.float().abs() + 2e-2)).max())
+        res_ok = bool(torch.equal(hro.cuda(), rout))
+        parity = {"residual_bitwise_vs_device_k2": res_ok, "output_max_abs_diff_vs_device_k2": float(d.max()),
+                  "ok": res_ok and worst <= 0.0}
+        del d
+    else:  # fp32: r' = x + r exactly, out vs a float64 restatement (the tests' 1e-5 bar)
+        xs, rs = hx.to("cuda", torch.float64), hr.to("cuda", torch.float64)
+        r64 = xs + rs
+        want = r64 * torch.rsqrt(r64.pow(2).mean(dim=1, keepdim=True) + EPS) * w.to(torch.float64)
+        err = float((ho.to("cuda", torch.float64) - want).abs().max())
+        parity = {"residual_bitwise": bool(torch.equal(hro.cuda(), (hx.cuda() + hr.cuda()))),
+                  "max_abs_err_output_vs_f64": err, "ok": err <= 1e-5}
+        del xs, rs, r64, want
     # median step: one slow step (host memory contention on a shared box)
     # moved a 20-step mean by 60 % once; mean / min / max are reported beside it
     return {"value": round(per[len(per) // 2], 2), "unit": UNIT, "h2d_bytes_per_step": 2 * nb + 4 * H,
             "d2h_bytes_per_step": 2 * nb, "steps": steps, "stat": "median of per-step CUDA-event times",
             "mean": round(sum(per) / len(per), 2), "min": round(per[0], 2), "max": round(per[-1], 2),
             "path": "tw_rmsnorm_residual_host (C-ABI via ctypes): pinned host input/residual -> chunked "
-                    "H2D | K2 | D2H pipeline over 3 streams -> pinned host output/residual_out"}
+                    "H2D | K2 | D2H pipeline over 3 streams -> pinned host output/residual_out",
+            "parity": parity}
+
+
+def k2_parity(bufs):
+    """The timed K2's results on the line's own inputs against a torch fp32
+    restatement of rmsnorm_residual (proj/src/numerics.cpp:30-64) at the
+    tests' bf16 bar: r' = RNE(x + r) bit for bit; out within 2e-2*|want| + 2e-2
+    (K2 normalises the bf16-rounded r', as does the restatement)."""
+    import torch
+    x, r, w, out, rout = bufs
+    worst, max_abs, res_ok = -1.0, 0.0, True
+    for a in range(0, x.shape[0], 1024):  # row blocks: bounded fp32 temporaries
+        rb = (x[a:a + 1024].float() + r[a:a + 1024].float()).to(torch.bfloat16)
+        res_ok &= bool(torch.equal(rout[a:a + 1024], rb))
+        rf = rb.float()
+        want = rf * torch.rsqrt(rf.pow(2).mean(dim=1, keepdim=True) + EPS) * w
+        d = (out[a:a + 1024].float() - want).abs()
+        worst = max(worst, float((d - (2e-2 * want.abs() + 2e-2)).max()))
+        max_abs = max(max_abs, float(d.max()))
+    return {"residual_bitwise": res_ok, "max_abs_err_output": round(max_abs, 5), "ok": res_ok and worst <= 0.0,
+            "bar": "r' = RNE(x + r) bitwise; |out - want| <= 2e-2*|want| + 2e-2",
+            "checker": "torch fp32 restatement on the device (not timed)"}
 
 
 def unfused_torch(T, H, flush, reps=20):
@@ -492,6 +531,7 @@ def run_ours_single(args):
                                              "lines, their write-back inside the event pair); the value above "
                                              "uses the write+read flush (clean L2)"},
         "clocks": clk.summary(),
+        "parity": k2_parity(bufs),
     }
     if not args.quick:
         line["e2e_dropin_f32"] = dict(e2e_f32, host_binding=numa)
