@@ -5,7 +5,8 @@
   latency    : tokens,default_ms,multimem_ms,nocomm_ms,fuseonly_ms,
                tokenweave_ms,tokenweave_speedup_x,fuseonly_speedup_x
 
-from profiles/sweep_r01.json (TP=1 op sweep) and profiles/weave_r01.json
+from profiles/sweep_rNN.json (TP=1 op sweep) and profiles/weave_rNN.json
+(`python tools/report.py r02`)
 (measured layers).  At TP=1 there is no AllReduce (0 us); `rmsnorm` is the
 unfused baseline on the same box (torch add + rms_norm) and `fused` is K2 on
 the whole GPU.  In `latency`, `multimem` is our unfused sequential layer
@@ -44,15 +45,16 @@ def latency(weave, model, tp):
 
 
 def main():
+    rnd = sys.argv[1] if len(sys.argv) > 1 else "r02"  # which round's sweep_/weave_ JSONs to render
     prof = os.path.join(ROOT, "profiles")
-    sweep = json.load(open(os.path.join(prof, "sweep_r01.json")))
-    weave = json.load(open(os.path.join(prof, "weave_r01.json")))
-    with open(os.path.join(prof, "microbench_tp1_r01.csv"), "w") as f:
+    sweep = json.load(open(os.path.join(prof, f"sweep_{rnd}.json")))
+    weave = json.load(open(os.path.join(prof, f"weave_{rnd}.json")))
+    with open(os.path.join(prof, f"microbench_tp1_{rnd}.csv"), "w") as f:
         f.write(microbench(sweep))
     for model, tp in (("llama-70b", 8), ("llama-70b", 1), ("mixtral-8x22b", 8)):
-        with open(os.path.join(prof, f"latency_{model}_tp{tp}shapes_r01.csv"), "w") as f:
+        with open(os.path.join(prof, f"latency_{model}_tp{tp}shapes_{rnd}.csv"), "w") as f:
             f.write(latency(weave, model, tp))
-    print(open(os.path.join(prof, "microbench_tp1_r01.csv")).read())
+    print(open(os.path.join(prof, f"microbench_tp1_{rnd}.csv")).read())
     return 0
 
 
