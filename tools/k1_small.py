@@ -64,10 +64,26 @@ def main():
                         comm.fused_allreduce_rmsnorm(T, H, shards, w, sm_budget=budget)
             torch.cuda.current_stream().wait_stream(s)
             graph10 = median_us(g.replay, reps=50)
+            # the same graph of K2 launches over the op's T rows with as many
+            # CTAs (W x budget) and no rank barriers: launch + row work, so
+            # graph_us_per_op - this = what the cross-rank barriers cost
+            x = torch.randn(T, H, device="cuda", dtype=torch.bfloat16)
+            r = torch.randn(T, H, device="cuda", dtype=torch.bfloat16)
+            o, ro = torch.empty_like(x), torch.empty_like(x)
+            g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(s):
+                tw.rmsnorm_residual(x, r, w[0], residual_out=ro, out=o, sm_budget=W * budget, stream=s)
+                with torch.cuda.graph(g2, stream=s):
+                    for _ in range(10):
+                        tw.rmsnorm_residual(x, r, w[0], residual_out=ro, out=o, sm_budget=W * budget, stream=s)
+            torch.cuda.current_stream().wait_stream(s)
+            floor10 = median_us(g2.replay, reps=50)
             row = {"tp": W, "T": T, "transport": args.transport,
                    "barrier_scope": "system" if os.environ.get("TW_FORCE_SYS_SCOPE") == "1" else "device",
                    "sm_budget_per_rank": budget, "eager_us": eager,
-                   "graph_us_per_op": round(graph10 / 10, 2)}
+                   "graph_us_per_op": round(graph10 / 10, 2),
+                   "k2_same_rows_graph_us_per_op": round(floor10 / 10, 2),
+                   "barrier_overhead_us": round((graph10 - floor10) / 10, 2)}
             print(json.dumps(row), flush=True)
             rows.append(row)
         torch.cuda.synchronize()
