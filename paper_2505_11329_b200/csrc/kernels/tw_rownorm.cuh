@@ -292,7 +292,9 @@ __device__ __forceinline__ void rank_barrier(const RowParams& p, const RankSlot&
         atomicExch(p.err, 1);
         break;
       }
-      __nanosleep(64);
+      // poll back to back first (a decode-size barrier completes within a few
+      // us), then back off so a long wait does not flood the memory system
+      if (spins > 256) __nanosleep(64);
     }
     if (exit) {
       // acquire: one ld.acquire of the counter the relaxed polls saw reach the
